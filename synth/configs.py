@@ -1,0 +1,94 @@
+"""Model shapes and layout configurations of the benchmark workloads.
+
+Shapes: Llama-3.1 config.json values [ext]; PAPER.md names the models only
+("LLaMA 3.1" 8B / 70B / 405B).  Layout configurations C1-C5 are
+BASELINE.json ``configs`` [0..4] (SURVEY.md §8 "Per-rank buffers").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, asdict
+
+
+@dataclass(frozen=True)
+class Model:
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    d_ffn: int
+    vocab: int
+    with_embed: int = 1
+
+    def replace(self, **kw) -> "Model":
+        d = asdict(self)
+        d.update(kw)
+        return Model(**d)
+
+
+MODELS = {
+    "toy": Model(2, 256, 8, 2, 32, 1024, 512, 1),
+    "llama3-8b": Model(32, 4096, 32, 8, 128, 14336, 128256, 1),
+    "llama3-70b": Model(80, 8192, 64, 8, 128, 28672, 128256, 1),
+    "llama3-405b": Model(126, 16384, 128, 8, 128, 53248, 128256, 1),
+    "llama3-405b-slice16": Model(16, 16384, 128, 8, 128, 53248, 128256, 0),
+}
+
+
+@dataclass(frozen=True)
+class LayoutConfig:
+    """One trainer->generator layout pair."""
+    name: str
+    model: str
+    fsdp: int
+    tp_train: int
+    tp_gen: int
+    src_dtype: str          # "f32" | "bf16"
+    dst_dtype: str          # "f32" | "bf16" | "fp8"
+    placement: str          # "disjoint" | "colocated" | "rotated"
+    fsdp_inner: bool = False
+    notes: str = ""
+
+    @property
+    def n_src(self) -> int:
+        return self.fsdp * self.tp_train
+
+    @property
+    def n_dst(self) -> int:
+        return self.tp_gen
+
+
+CONFIGS = {
+    "c1": LayoutConfig("c1", "toy", 2, 1, 2, "f32", "bf16", "disjoint",
+                       notes="toy fp32 FSDP=2 -> bf16 TP=2"),
+    "c2": LayoutConfig("c2", "llama3-8b", 4, 1, 4, "f32", "bf16", "disjoint",
+                       notes="8B fp32 FSDP=4 (GPUs 0..G/2) -> bf16 TP=4 (GPUs G/2..G)"),
+    "c3": LayoutConfig("c3", "llama3-70b", 8, 1, 8, "bf16", "bf16", "colocated",
+                       notes="70B bf16 FSDP=8 -> bf16 TP=8, co-located"),
+    "c4": LayoutConfig("c4", "llama3-70b", 1, 8, 8, "bf16", "fp8", "colocated",
+                       notes="70B bf16 TP=8 -> fp8 TP=8 with 128x128 block scales"),
+    "c5": LayoutConfig("c5", "llama3-405b-slice16", 2, 4, 8, "bf16", "bf16", "colocated",
+                       notes="405B 16-layer slice FSDP=2xTP=4 -> TP=8, TP-innermost mesh"),
+}
+
+
+def placement(cfg: LayoutConfig, n_gpus: int):
+    """Logical rank -> GPU ordinal maps (src_device[], dst_device[]).
+
+    SURVEY.md §8(d) "Placements": C2 uses disjoint halves for G >= 2 (trainer
+    ranks block-mapped onto GPUs [0, G/2), generator onto [G/2, G)) and all on
+    GPU 0 at G = 1; co-located configs map logical rank r -> GPU floor(r*G/n)
+    on both sides; "rotated" shifts the trainer by one GPU.
+    """
+    ns, nd = cfg.n_src, cfg.n_dst
+    if n_gpus == 1:
+        return [0] * ns, [0] * nd
+    if cfg.placement == "disjoint":
+        half = n_gpus // 2
+        return ([r * half // ns for r in range(ns)],
+                [half + g * (n_gpus - half) // nd for g in range(nd)])
+    src = [r * n_gpus // ns for r in range(ns)]
+    dst = [g * n_gpus // nd for g in range(nd)]
+    if cfg.placement == "rotated":
+        src = [(d + 1) % n_gpus for d in src]
+    return src, dst

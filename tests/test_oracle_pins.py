@@ -1,0 +1,260 @@
+"""Pins of the CPU oracle against things other than itself.
+
+* bf16 RNE: exhaustive over all 2^32 fp32 patterns against ml_dtypes, plus a
+  torch CPU sample (two independent library routines); NaN compared as a class
+  (reading R6).
+* e4m3 (E4M3FN, RN, satfinite): exhaustive over every fp32 with |x| < 464
+  against ml_dtypes (non-saturating libraries and satfinite agree there,
+  reading R7); saturation checked on the closed form (448).
+* fp8 block quantisation: numpy fp32 arithmetic + ml_dtypes cast (tests/brute.py)
+  on random and special blocks.
+* layout + whole sync: independent brute force (torch.chunk / torch.cat /
+  ml_dtypes) over the 80-combination toy sweep and odd layouts; closed-form
+  provenance; dst coverage exactly once; error codes.
+* parameter counts: the public Llama-3.1 sizes (tests/golden/param_counts.txt).
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+
+import ml_dtypes
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from synth import MODELS
+from tests import brute
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------------- casts
+
+def _bf16_chunk(start, n):
+    x = (np.arange(n, dtype=np.uint64) + np.uint64(start)).astype(np.uint32)
+    got = oracle.bf16_rne(x)
+    with np.errstate(invalid="ignore"):
+        ref = x.view(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    nan_in = np.isnan(x.view(np.float32))
+    got_nan = ((got & 0x7F80) == 0x7F80) & ((got & 0x7F) != 0)
+    bad = (got != ref) & ~nan_in
+    return int(bad.sum()), bool(got_nan[nan_in].all())
+
+
+def test_bf16_rne_exhaustive_vs_ml_dtypes(oracle_lib):
+    n = 1 << 24
+    with cf.ThreadPoolExecutor(8) as ex:
+        res = list(ex.map(lambda s: _bf16_chunk(s, n), range(0, 1 << 32, n)))
+    assert sum(r[0] for r in res) == 0
+    assert all(r[1] for r in res)
+
+
+def test_bf16_rne_vs_torch_and_special_cases(oracle_lib):
+    rng = np.random.default_rng(1)
+    x = rng.integers(0, 1 << 32, size=1 << 22, dtype=np.uint64).astype(np.uint32)
+    x = x[~np.isnan(x.view(np.float32))]
+    ref = torch.from_numpy(x.view(np.float32).copy()).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(oracle.bf16_rne(x), ref)
+    # SURVEY App. B probes: ties to even, subnormal rounding, overflow to Inf
+    cases = {0x3F808000: 0x3F80, 0x3F818000: 0x3F82, 0x00038000: 0x0004, 0x7F7F8000: 0x7F80,
+             0x80008000: 0x8000, 0x00008001: 0x0001, 0x7F7FFFFF: 0x7F80, 0xFF800000: 0xFF80}
+    for k, v in cases.items():
+        assert oracle.bf16_rne(np.array([k], np.uint32))[0] == v, hex(k)
+
+
+def _e4m3_chunk(start, n):
+    x = (np.arange(n, dtype=np.uint64) + np.uint64(start)).astype(np.uint32)
+    f = x.view(np.float32)
+    keep = np.abs(f) < 464
+    f = f[keep]
+    got = oracle.e4m3(f)
+    ref = f.astype(ml_dtypes.float8_e4m3fn).view(np.uint8)
+    return int((got != ref).sum())
+
+
+def test_e4m3_exhaustive_below_464_vs_ml_dtypes(oracle_lib):
+    limit = int(np.array([464.0], np.float32).view(np.uint32)[0])   # 0x43E80000
+    n = 1 << 24
+    starts = list(range(0, limit, n)) + list(range(0x80000000, 0x80000000 + limit, n))
+    with cf.ThreadPoolExecutor(8) as ex:
+        assert sum(ex.map(lambda s: _e4m3_chunk(s, n), starts)) == 0
+
+
+def test_e4m3_saturation_and_specials(oracle_lib):
+    f = np.array([448.0, 449.0, 464.0, 465.0, 1e30, -1e30, -500.0, 2.0 ** -10, 1.5 * 2.0 ** -10,
+                  2.0 ** -9, -2.0 ** -9, 2.0 ** -6, 0.0, -0.0, 1e-45, -1e-45], np.float32)
+    want = [0x7E, 0x7E, 0x7E, 0x7E, 0x7E, 0xFE, 0xFE, 0x00, 0x01, 0x01, 0x81, 0x08, 0x00, 0x80, 0x00, 0x80]
+    assert oracle.e4m3(f).tolist() == want
+    assert oracle.e4m3(np.array([np.nan], np.float32))[0] & 0x7F == 0x7F
+
+
+@pytest.mark.parametrize("kind", ["random", "zero", "outlier", "ties", "subnormal_out", "partial", "tiny"])
+def test_fp8_block_vs_numpy_ml_dtypes(oracle_lib, kind):
+    rng = np.random.default_rng(7)
+    shape = (128, 128)
+    if kind == "random":
+        x = rng.normal(0, 0.02, shape).astype(np.float32)
+    elif kind == "zero":
+        x = np.zeros(shape, np.float32)
+        x[3, 5] = -0.0
+    elif kind == "outlier":
+        x = rng.normal(0, 0.02, shape).astype(np.float32)
+        x[17, 99] = -37.5
+    elif kind == "ties":
+        # amax 448 -> inv = 1: values exactly halfway between e4m3 neighbours
+        x = rng.choice(np.array([1.0625, 1.1875, 2.125, 3.25, 9.5, 0.0029296875, -1.0625, 448.0], np.float32), shape)
+    elif kind == "subnormal_out":
+        x = rng.normal(0, 1e-4, shape).astype(np.float32)
+        x[0, 0] = 1.0
+    elif kind == "partial":
+        shape = (64, 96)
+        x = rng.normal(0, 0.02, shape).astype(np.float32)
+    else:  # amax below the 2^-64 floor
+        x = (rng.normal(0, 1, shape) * 1e-30).astype(np.float32)
+    q, s = oracle.fp8_block(x)
+    q_ref, s_ref = brute.fp8_quant(x)
+    assert s == s_ref[0, 0]
+    assert np.array_equal(q, q_ref)
+
+
+# --------------------------------------------------------------------------- layout / sync
+
+def _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src, sentinel=0):
+    L = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, inner)
+    assert L.status == 0
+    dst = [np.full(L.dst_rank_bytes(g), sentinel, np.uint8) for g in range(tpg)]
+    rc = L.sync(src, dst)
+    assert rc == 0, rc
+    return L, dst
+
+
+SWEEP = [(f, tt, tg) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)]
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg", SWEEP)
+def test_oracle_vs_brute_toy_sweep_bf16(oracle_lib, fsdp, tpt, tpg):
+    m = MODELS["toy"].replace(n_layers=1)
+    src, want = brute.build(m, 3, fsdp, tpt, tpg, "f32", "bf16")
+    L = oracle.Layout(m, fsdp, tpt, tpg, "f32", "bf16")
+    assert [L.src_rank_bytes(r) for r in range(fsdp * tpt)] == [b.size for b in src]
+    _, dst = _run_oracle(m, fsdp, tpt, tpg, "f32", "bf16", False, src)
+    assert [d.size for d in dst] == [w.size for w in want]
+    for d, w in zip(dst, want):
+        assert np.array_equal(d, w)
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
+    (2, 1, 2, "f32", "bf16", False),      # C1
+    (3, 1, 4, "f32", "fp8", False),       # multi-source fp8 blocks
+    (2, 2, 8, "bf16", "fp8", False),      # multi-source blocks + KV replication
+    (2, 2, 8, "bf16", "fp8", True),       # FSDP-innermost mesh
+    (1, 8, 8, "bf16", "fp8", False),      # C4 shape class
+    (8, 1, 8, "bf16", "bf16", False),     # C3 shape class
+    (2, 4, 8, "bf16", "bf16", False),     # C5 shape class
+    (2, 4, 8, "bf16", "bf16", True),
+    (3, 2, 4, "f32", "f32", False),       # identity cast (provenance mode)
+    (4, 1, 1, "f32", "bf16", False),
+])
+def test_oracle_vs_brute_odd_layouts(oracle_lib, fsdp, tpt, tpg, sdt, ddt, inner):
+    m = MODELS["toy"]
+    src, want = brute.build(m, 5, fsdp, tpt, tpg, sdt, ddt, inner)
+    _, dst = _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src)
+    for d, w in zip(dst, want):
+        assert np.array_equal(d, w)
+
+
+def test_oracle_provenance_closed_form(oracle_lib):
+    """f32 -> f32 identity: every generator element equals the generator value of
+    the source coordinate given in closed form by readings R4 (no brute force)."""
+    m = MODELS["toy"]
+    fsdp, tpt, T = 3, 2, 8
+    src, _ = brute.build(m, 11, fsdp, tpt, T, "f32", "f32")
+    L, dst = _run_oracle(m, fsdp, tpt, T, "f32", "f32", False, src)
+    hd, H, KV, d, f, V = m.head_dim, m.n_heads, m.n_kv_heads, m.d_model, m.d_ffn, m.vocab
+    for g in range(T):
+        for gp in range(L.n_dst_params):
+            R, C, _, off, _ = L.dst_param(g, gp)
+            got = dst[g][off:off + R * C * 4].view(np.uint32).reshape(R, C)
+            rr = np.arange(R)[:, None]
+            cc = np.arange(C)[None, :]
+            # generator param gp -> (source param(s), closed-form coordinates)
+            if gp == 0:                       # embed: vocab rows g*V/T + r
+                exp = synth.weight_bits(11, 0, False, "f32", g * (V // T) + rr, cc)
+            elif gp == L.n_dst_params - 2:    # final_norm
+                exp = synth.weight_bits(11, L.n_src_params - 2, True, "f32", rr, cc)
+            elif gp == L.n_dst_params - 1:    # lm_head
+                exp = synth.weight_bits(11, L.n_src_params - 1, False, "f32", g * (V // T) + rr, cc)
+            else:
+                l, s = divmod(gp - 1, 6)
+                base = 1 + 9 * l
+                if s in (0, 3):               # norms: full copy
+                    exp = synth.weight_bits(11, base + (0 if s == 0 else 5), True, "f32", rr, cc)
+                elif s == 1:                  # qkv
+                    qr = H * hd // T
+                    head = g // (T // KV)     # T > KV here: replicated whole KV head
+                    exp = np.where(rr < qr, synth.weight_bits(11, base + 1, False, "f32", g * qr + rr, cc),
+                                   np.where(rr < qr + hd,
+                                            synth.weight_bits(11, base + 2, False, "f32", head * hd + rr - qr, cc),
+                                            synth.weight_bits(11, base + 3, False, "f32", head * hd + rr - qr - hd, cc)))
+                elif s == 2:                  # o: input columns g*H*hd/T + c
+                    exp = synth.weight_bits(11, base + 4, False, "f32", rr, g * (H * hd // T) + cc)
+                elif s == 4:                  # gate_up
+                    fr = f // T
+                    exp = np.where(rr < fr, synth.weight_bits(11, base + 6, False, "f32", g * fr + rr, cc),
+                                   synth.weight_bits(11, base + 7, False, "f32", g * fr + rr - fr, cc))
+                else:                         # down
+                    exp = synth.weight_bits(11, base + 8, False, "f32", rr, g * (f // T) + cc)
+            assert np.array_equal(got, exp), (g, gp)
+
+
+def test_oracle_dst_coverage_exactly_once(oracle_lib):
+    """Two runs with different sentinels: bytes that differ were never written.
+    They must be exactly the alignment padding between parameter pieces."""
+    m = MODELS["toy"]
+    for cfg in [(3, 2, 8, "bf16", "fp8"), (2, 1, 2, "f32", "bf16")]:
+        src, _ = brute.build(m, 2, cfg[0], cfg[1], cfg[2], cfg[3], cfg[4])
+        L, a = _run_oracle(m, *cfg, False, src, sentinel=0x00)
+        _, b = _run_oracle(m, *cfg, False, src, sentinel=0xFF)
+        for g in range(cfg[2]):
+            covered = np.zeros(a[g].size, bool)
+            for gp in range(L.n_dst_params):
+                R, C, q, off, soff = L.dst_param(g, gp)
+                es = 1 if q else {"f32": 4, "bf16": 2, "fp8": 2}[cfg[4]]
+                assert not covered[off:off + R * C * es].any()
+                covered[off:off + R * C * es] = True
+                if q:
+                    n = -(-R // 128) * -(-C // 128) * 4
+                    assert not covered[soff:soff + n].any()
+                    covered[soff:soff + n] = True
+            written = a[g] == b[g]
+            assert np.array_equal(written, covered)
+
+
+def test_oracle_errors(oracle_lib):
+    m = MODELS["toy"]
+    assert oracle.Layout(m, 1, 1, 3, "f32", "bf16").status == oracle.E_INDIVISIBLE     # H % 3
+    assert oracle.Layout(m, 1, 1, 16, "f32", "bf16").status == oracle.E_INDIVISIBLE    # H=8 % 16
+    assert oracle.Layout(m, 1, 3, 2, "f32", "bf16").status == oracle.E_INDIVISIBLE     # trainer TP 3
+    assert oracle.Layout(m, 1, 1, 2, "bf16", "f32").status == oracle.E_UNSUPPORTED
+    # replicas that differ: norms are replicated over trainer TP ranks
+    src, _ = brute.build(m, 1, 1, 2, 2, "f32", "bf16")
+    L = oracle.Layout(m, 1, 2, 2, "f32", "bf16")
+    off = L.src_piece(1, 1)[0]                # l0.attn_norm on rank 1
+    src[1][off] ^= 1
+    dst = [np.zeros(L.dst_rank_bytes(g), np.uint8) for g in range(2)]
+    assert L.sync(src, dst) == oracle.E_MISMATCH
+
+
+def test_param_counts_match_public_llama_sizes(oracle_lib):
+    """tests/golden/param_counts.txt: Llama-3.1 public parameter counts [ext]
+    (SURVEY.md §8 shapes table); the oracle's parameter list must sum to them."""
+    for line in open(os.path.join(GOLDEN, "param_counts.txt")):
+        if not line.strip() or line.startswith("#"):
+            continue
+        name, count = line.split()
+        L = oracle.Layout(MODELS[name], 1, 1, 1)
+        total = sum(L.src_param_info(p)[0] * L.src_param_info(p)[1] for p in range(L.n_src_params))
+        assert total == int(count), name
