@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py -- DDMA trainer->generator weight-sync latency on B200 (LlamaRL,
+arxiv 2505.24034 §5.2; BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W --config c2]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+  python bench.py --impl reference ...      # the CPU oracle on host cores
+
+A step is one whole sync of the configuration's
+full model: every trainer shard read, every generator shard written.  At N=1
+the workload is configs[1] (C2, Llama-3.1 8B fp32 FSDP=4 -> bf16 TP=4, all
+logical ranks on GPU 0); at N>1 the same model with trainer ranks on GPUs
+[0, N/2) and generator ranks on [N/2, N), i.e. strong scaling.
+Inputs (GBs) are larger than the 126 MB L2, so no flush is needed between
+steps.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "weight-sync latency (ms) and NVLink GB/s/GPU for Llama-3 8B/70B at 1/2/4/8 B200"
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                      "-i", ",".join(map(str, self.gpus))], capture_output=True, text=True,
+                                     timeout=5).stdout
+                for line in out.strip().splitlines():
+                    f = [x.strip() for x in line.split(",")]
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        load = [s for s in self.samples if num(s[-1]) and num(s[-1]) > 0] or self.samples
+        sm = sorted(num(s[1]) for s in load if num(s[1]) is not None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in load for n, v in zip(names, s[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": num(load[0][2]), "reasons": reasons,
+                "samples": len(load)}
+
+
+def _dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _allmax(x):
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _allsum(x):
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def _barrier():
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- CPU oracle legs
+
+def _oracle_sample(cfg_name, seed=0):
+    """A bounded sample of the workload for the CPU oracle: ONE decoder layer of the
+    config's model (no embed / lm_head), same layout parameters.  Returns
+    (oracle layout, src buffers, fraction of the full model's elements)."""
+    import numpy as np
+    import oracle
+    from synth import MODELS, CONFIGS
+    cfg = CONFIGS[cfg_name]
+    full = MODELS[cfg.model]
+    m = full.replace(n_layers=1, with_embed=0)
+    ol = oracle.Layout(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
+    rng = np.random.default_rng(seed)
+    src = []
+    for r in range(ol.n_src):
+        n = ol.src_rank_bytes(r)
+        if cfg.src_dtype == "f32":
+            src.append((rng.standard_normal(n // 4, dtype=np.float32) * np.float32(0.02)).view(np.uint8))
+        else:
+            x = (rng.standard_normal(n // 2, dtype=np.float32) * np.float32(0.02)).view(np.uint32) >> 16
+            src.append(x.astype(np.uint16).view(np.uint8))
+    def count(mm):
+        L = oracle.Layout(mm, 1, 1, 1)
+        return sum(L.src_param_info(p)[0] * L.src_param_info(p)[1] for p in range(L.n_src_params))
+    frac = count(m) / count(full)
+    return ol, src, frac
+
+
+def _time_oracle_once(ol, src):
+    import numpy as np
+    dst = [np.zeros(ol.dst_rank_bytes(g), np.uint8) for g in range(ol.n_dst)]
+    t0 = time.perf_counter()
+    rc = ol.sync(src, dst)
+    dt = time.perf_counter() - t0
+    assert rc == 0, rc
+    return dt
+
+
+def cpu_baseline(cfg_name, full_model_name):
+    ol, src, frac = _oracle_sample(cfg_name)
+    dt = _time_oracle_once(ol, src)
+    return {"value": round(dt / frac * 1e3, 3), "unit": "ms", "cores": 1, "kind": "oracle",
+            "sample": f"1 decoder layer of {full_model_name} ({frac * 100:.2f}% of the elements), "
+                      f"oracle/oracle.c single-threaded on {os.cpu_count()} host cores; "
+                      f"{dt:.2f} s measured, extrapolated linearly to the whole model"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as it stands on the host (rank 0 only)."""
+    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    ol, src, frac = _oracle_sample(args.config)
+    for _ in range(args.warmup):
+        _time_oracle_once(ol, src)
+    ts = [_time_oracle_once(ol, src) for _ in range(args.steps)]
+    step_ms = sum(ts) / len(ts) / frac * 1e3
+    sample = (f"1 decoder layer of {cfg.model} per step ({frac * 100:.2f}% of the elements), "
+              f"extrapolated linearly to the whole model; oracle/oracle.c single-threaded")
+    line = {"impl": "reference", "metric": METRIC, "value": round(step_ms, 3), "unit": "ms",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}",
+            "data": "synthetic", "config": {"workload": _workload_name(cfg, args.gpus), "layout": cfg.notes},
+            "cpu_baseline": {"value": round(step_ms, 3), "unit": "ms", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(step_ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _workload_name(cfg, n):
+    return f"{cfg.name}: {cfg.notes} @ {n} GPU(s)"
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_llrl(args):
+    import torch
+    from paper_2505_24034_b200 import build
+    build.build()
+    from paper_2505_24034_b200 import runner
+    world, rank, local = _dist_setup(args)
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    spec = runner.spec_for(args.config, args.gpus)
+    job = runner.SyncJob(spec, device=local, seed=0)
+    cfg = job.cfg
+    stream = job.stream
+
+    # warm-up (also uploads the device tables)
+    for _ in range(args.warmup):
+        job.sync()
+    _barrier()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler([local]) as clk:
+        time.sleep(0.25)       # let the sampler start before the timed region
+        _barrier()
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(args.steps):
+                job.sync()
+                ev[k + 1].record(stream)
+        _barrier()
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    ms = _allmax(total_ms / args.steps)
+    ms_min = _allmax(min(step_ms))
+    launches = int(_allsum(job.num_launches() * args.steps))
+
+    # roofline: algorithmic bytes of this device's kernels per launch / their duration
+    hbm_peak, peak_src = _peaks()
+    b = job.plan.device_bytes(job.device)
+    hbm_bytes = b["hbm_read"] + b["hbm_write"]
+    nvl_bytes = max(b["nvl_tx"], b["nvl_rx"])
+    t_hbm = _allmax(hbm_bytes / hbm_peak / 1e6)            # ms
+    t_nvl = _allmax(nvl_bytes / NVLINK_PEER_GBS / 1e6)
+    my_ms = total_ms / args.steps
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": round(nvl_bytes / my_ms / 1e6, 1), "peak": NVLINK_PEER_GBS,
+                "unit": "GB/s", "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
+    else:
+        roof = {"bound": "hbm", "achieved": round(hbm_bytes / my_ms / 1e6, 1), "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": peak_src}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["traffic"] = _ncu_traffic(args.config, args.gpus)
+    roof["kernel"] = "llrl_k_sync (relayout+cast push; whole sync of rank 0's device)"
+    roof["t_lb_ms"] = round(max(t_hbm, t_nvl), 3)
+
+    # end to end through the C ABI with host buffers (pinned), copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(job, args)
+
+    tot = job.plan.stats()
+    tr = job.plan.traffic()
+    wire = sum(tr[i][j] for i in range(len(tr)) for j in range(len(tr)) if i != j)
+    nvl_per_gpu = _allmax(max(b["nvl_tx"], b["nvl_rx"]) / (ms * 1e6)) if wire else 0.0
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "ms_min": round(ms_min, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": "synthetic (counter-based Llama-init-scale weights)",
+            "config": {"workload": _workload_name(cfg, args.gpus), "model": cfg.model,
+                       "layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
+                       "tp_gen": cfg.tp_gen, "placement": cfg.placement,
+                       "l2": "inputs >> 126 MB L2 (no flush needed)"},
+            "throughput": {"gen_bytes_per_s_GB": round(tot.dst_bytes / (ms * 1e6), 1),
+                           "algorithmic_bytes_GB": round((tot.src_bytes + tot.dst_bytes) / 1e9, 3),
+                           "nvlink_wire_GB": round(wire / 1e9, 3),
+                           "nvlink_GBps_per_gpu_max": round(nvl_per_gpu, 1)},
+            "roofline": roof,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.config, cfg.model)
+        print(json.dumps(line), flush=True)
+    job.close()
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _e2e(job, args):
+    import torch
+    host_src = {r: torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for r, t in job.src.items()}
+    host_dst = {g: torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for g, t in job.dst.items()}
+    for r, t in job.src.items():
+        host_src[r].copy_(t)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    job.sync_host(host_src, host_dst)
+    _barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(job.stream)
+    for _ in range(steps):
+        job.sync_host(host_src, host_dst)
+    e1.record(job.stream)
+    _barrier()
+    ms = _allmax(e0.elapsed_time(e1) / steps)
+    h2d = int(_allsum(sum(t.numel() for t in host_src.values())))
+    d2h = int(_allsum(sum(t.numel() for t in host_dst.values())))
+    return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": steps, "api": "llrl_sync_host (C ABI, pinned host buffers)"}
+
+
+def _ncu_traffic(config, n):
+    """dram read+write bytes per launch from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(f"{config}@{n}")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="llrl", choices=["llrl", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_llrl(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,210 @@
+/*
+ * llrl.h -- C ABI of libllrl: B200-native DDMA weight synchronisation
+ * (LlamaRL, arxiv 2505.24034, §5.2 "Distributed Direct Memory Access
+ * (DDMA) Weights Update").
+ *
+ * The problem: "sending updated policy parameters from a training
+ * executor to an inference executor", where "each GPU only stores or updates
+ * its assigned shards, leveraging the same tensor and parallel groups used
+ * during training", by "direct memory transfers between CUDA memory
+ * regions across devices -- bypassing CPU memory".  Trainer and
+ * generator "can use different parallelisms and data precision",
+ * including "quantization (fp8 ...) on the inference side".
+ *
+ * Three calls carry the method:
+ *   llrl_layout_describe  -- step a1: both sides' per-rank flat-buffer layouts
+ *   llrl_plan_create      -- step a2: the integer routing plan (tiles -> runs)
+ *   llrl_sync             -- steps a3-a6: the hot path on one device's stream
+ * Conventions that the paper leaves open are DESIGN.md readings R0-R11.
+ *
+ * General rules
+ *   - Every call returns llrl_status (0 = OK, negative = error) unless noted;
+ *     on error llrl_last_error() returns a thread-local message.  No C++
+ *     exception or abort crosses the ABI.
+ *   - Offsets in llrl_param_view are BYTES from the rank buffer base.  Offsets
+ *     in llrl_run are ELEMENTS of that side's data dtype.
+ *   - Rank buffers must be 256-byte aligned device allocations owned by the
+ *     caller.  The library owns layouts, plans and comms until *_destroy,
+ *     including their device-side tables and flag buffers.
+ *   - `cudaStream_t` is passed as `void *` so this header has no CUDA
+ *     dependency.
+ */
+#ifndef LLRL_H
+#define LLRL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LLRL_OK = 0,
+    LLRL_E_INVALID = -1,      /* bad argument / NULL / out of range          */
+    LLRL_E_INDIVISIBLE = -2,  /* a TP split does not divide a dimension (R1, R4) */
+    LLRL_E_MISMATCH = -3,     /* src and dst layouts describe different models */
+    LLRL_E_UNSUPPORTED = -4,  /* dtype combination not supported             */
+    LLRL_E_CUDA = -5,         /* CUDA runtime error (message has cudaGetErrorString) */
+    LLRL_E_NOPEER = -6,       /* a device the plan needs has no comm peer mapping */
+    LLRL_E_NOMEM = -7         /* host or device allocation failed            */
+} llrl_status;
+
+typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2 } llrl_dtype;
+
+/* Llama-style decoder shapes (Llama-3.1 config.json fields [ext]). */
+typedef struct {
+    int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, with_embed;
+} llrl_model;
+
+/* flags of llrl_layout_describe */
+#define LLRL_MESH_FSDP_INNER 1u   /* trainer rank = t*fsdp + f (default f*tp + t), R3 */
+
+/* parameter kinds reported by llrl_layout_param_view */
+enum {
+    LLRL_P_ATTN_NORM = 0, LLRL_P_Q, LLRL_P_K, LLRL_P_V, LLRL_P_O, LLRL_P_MLP_NORM,
+    LLRL_P_GATE, LLRL_P_UP, LLRL_P_DOWN, LLRL_P_EMBED, LLRL_P_FINAL_NORM, LLRL_P_LM_HEAD,
+    LLRL_P_QKV, LLRL_P_GATE_UP
+};
+
+typedef struct llrl_layout llrl_layout;
+typedef struct llrl_plan llrl_plan;
+typedef struct llrl_comm llrl_comm;
+
+/* One parameter piece on one rank. */
+typedef struct {
+    int32_t kind;        /* LLRL_P_* */
+    int32_t layer;       /* -1 for embed / final_norm / lm_head */
+    int32_t dtype;       /* llrl_dtype of the data */
+    int32_t quantised;   /* 1: fp8 data followed by an fp32 scale grid (R7, R9) */
+    int64_t rows, cols;  /* local shape, row-major, leading dimension = cols */
+    int64_t byte_off;    /* data offset in the rank buffer */
+    int64_t scale_off;   /* scale grid offset, -1 if not quantised */
+    int64_t full_r0, full_c0;  /* src side: top-left of the piece in the full tensor; dst: 0 */
+    int32_t src_param;   /* src side: canonical source-param id; dst side: -1 */
+    int32_t is_norm;
+} llrl_param_view;
+
+/* ---- a1: layouts ------------------------------------------------------------
+ * Describe the trainer (src) and generator (dst) layouts of `m` for a trainer
+ * mesh fsdp x tp_train (fsdp*tp_train ranks, R1-R3) and a generator with
+ * tp_gen ranks (R4).  src_dtype in {F32, BF16}; dst_dtype in {F32 (only from
+ * F32: identity/provenance mode), BF16, FP8_E4M3 (R7)}.
+ * Errors: INVALID (NULL, non-positive sizes), INDIVISIBLE, UNSUPPORTED.
+ * Ownership: *src_out and *dst_out belong to the caller (llrl_layout_destroy). */
+llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
+                                 llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
+                                 llrl_layout **src_out, llrl_layout **dst_out);
+llrl_status llrl_layout_num_ranks(const llrl_layout *l, int *n);
+llrl_status llrl_layout_num_params(const llrl_layout *l, int *n);
+/* Bytes of rank `rank`'s flat buffer (a multiple of 256). */
+llrl_status llrl_layout_rank_bytes(const llrl_layout *l, int rank, int64_t *bytes);
+/* Where parameter `param` (canonical index of that side, R0) lives on `rank`. */
+llrl_status llrl_layout_param_view(const llrl_layout *l, int rank, int param, llrl_param_view *out);
+void llrl_layout_destroy(llrl_layout *l);
+
+/* ---- a2: plan --------------------------------------------------------------
+ * Build the routing plan from src to dst (same model; else MISMATCH).
+ * src_device[r] / dst_device[g] = GPU ordinal hosting trainer rank r /
+ * generator rank g (any mapping; several ranks may share a GPU).  Host-only:
+ * no CUDA call is made; device tables are uploaded on the first llrl_sync
+ * that needs them.  flags: 0 (reserved).
+ * Ownership: the plan copies what it needs; the layouts may be destroyed. */
+llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst,
+                             const int *src_device, const int *dst_device, uint32_t flags,
+                             llrl_plan **out);
+void llrl_plan_destroy(llrl_plan *p);
+
+/* A canonical 1-D run: `len` consecutive elements (verification view). */
+typedef struct {
+    int32_t src_param;   /* canonical source-param id */
+    int32_t src_rank, dst_rank;
+    int32_t flags;       /* bit0: quantised destination (fp8 bytes) */
+    int64_t src_off, dst_off, len;   /* elements of each side's data dtype */
+} llrl_run;
+llrl_status llrl_plan_num_runs(const llrl_plan *p, int64_t *n);
+llrl_status llrl_plan_get_runs(const llrl_plan *p, int64_t first, int64_t count, llrl_run *out);
+
+typedef struct {
+    int32_t n_devices;          /* 1 + the largest device ordinal used      */
+    int32_t n_src_ranks, n_dst_ranks;
+    int64_t n_tiles;            /* rectangle intersections (param, src, dst) */
+    int64_t n_items;            /* work items over all devices              */
+    int64_t n_fp8_blocks, n_fp8_pull_blocks;
+    int64_t src_bytes, dst_bytes;   /* algorithmic bytes read / written (whole sync) */
+} llrl_plan_stats;
+llrl_status llrl_plan_stats_get(const llrl_plan *p, llrl_plan_stats *out);
+/* bytes_GxG[s*G + d] = bytes written by device s's work into device d's memory
+ * (wire bytes when s != d; local HBM writes when s == d).  G = n_devices. */
+llrl_status llrl_plan_traffic(const llrl_plan *p, int64_t *bytes_GxG);
+/* Algorithmic HBM bytes of one device for one sync: reads of everything sourced
+ * there plus writes of everything landing there; and NVLink egress/ingress. */
+llrl_status llrl_plan_device_bytes(const llrl_plan *p, int device, int64_t *hbm_read,
+                                   int64_t *hbm_write, int64_t *nvl_tx, int64_t *nvl_rx);
+
+/* ---- completion comm (a6) --------------------------------------------------
+ * A comm owns one 256-byte flag buffer on `device` (epoch counters, R10).
+ * Devices that exchange data in a plan must know each other's flag buffers:
+ *   multi-process: llrl_comm_export on each, exchange the 64-byte handles
+ *                  (e.g. torch.distributed.all_gather_object), llrl_comm_import;
+ *   single process: llrl_comm_flag_ptr + llrl_comm_set_peer (peer access is
+ *                  enabled by the library).
+ * One comm per device per process; it may serve any number of plans, provided
+ * every process issues the same sequence of llrl_sync calls. */
+llrl_status llrl_comm_create(int device, llrl_comm **out);
+llrl_status llrl_comm_export(const llrl_comm *c, void *handle64);
+llrl_status llrl_comm_import(llrl_comm *c, int peer_device, const void *handle64);
+llrl_status llrl_comm_flag_ptr(const llrl_comm *c, void **dev_ptr);
+llrl_status llrl_comm_set_peer(llrl_comm *c, int peer_device, void *peer_flag_dev_ptr);
+void llrl_comm_destroy(llrl_comm *c);
+
+/* ---- IPC helpers for caller-owned buffers ----------------------------------
+ * handle64 + byte offset of `dev_ptr` inside its cudaMalloc allocation, and
+ * the reverse mapping in another process (peer access over NVLink). */
+llrl_status llrl_ipc_handle(const void *dev_ptr, void *handle64, int64_t *offset);
+llrl_status llrl_ipc_open(const void *handle64, int64_t offset, void **dev_ptr);
+llrl_status llrl_ipc_close(void *dev_ptr, int64_t offset);
+
+/* ---- a3-a6: the hot path ----------------------------------------------------
+ * Enqueue on `stream` (a cudaStream_t of device comm->device) every work item
+ * this device executes: push items for tiles sourced here (cast before the
+ * transfer: wire bytes at the destination width), pull items for multi-source
+ * fp8 blocks landing here (R8); then signal each destination device this device
+ * wrote to; then wait until every device writing into this device's
+ * destinations has signalled.  When `stream` passes that point, every
+ * generator shard resident on this device is complete.  Asynchronous to the
+ * host; no host round trip on the per-step path.
+ * src_ptrs[r] (r < n_src_ranks), dst_ptrs[g] (g < n_dst_ranks): rank buffer
+ * base pointers valid in this process (local or peer/IPC-mapped); entries this
+ * device never touches may be NULL.  `comm` may be NULL iff the plan uses one
+ * device.  Preconditions (step boundary): no one writes the src
+ * buffers or reads the dst buffers during the sync.
+ * Errors: INVALID, NOPEER (a needed peer flag buffer or pointer missing), CUDA. */
+llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device,
+                      void *const *src_ptrs, void *const *dst_ptrs, void *stream);
+
+/* Same as llrl_sync, with the trainer shards hosted on this device first
+ * copied from HOST buffers host_src[r] and, after the sync, the generator
+ * shards resident on this device copied back to host_dst[g] (entries of ranks
+ * on other devices are ignored; host buffers should be pinned).  The copies are
+ * pipelined with the kernels in chunks.  Device buffers as in llrl_sync. */
+llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device,
+                           const void *const *host_src, void *const *host_dst,
+                           void *const *src_ptrs, void *const *dst_ptrs, void *stream);
+
+/* Number of kernels llrl_sync enqueues on `device` (for launch accounting). */
+llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n);
+
+/* ---- harness support (tests / bench only; not part of the method) ----------
+ * K0: fill trainer rank `rank`'s buffer with the counter-based synthetic
+ * weights of DESIGN.md §4 (bit-identical to synth.weight_bits). */
+llrl_status llrl_fill_synthetic(const llrl_layout *src, int rank, void *dev_ptr, uint64_t seed,
+                                void *stream);
+
+const char *llrl_last_error(void);
+const char *llrl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LLRL_H */

@@ -1,0 +1,177 @@
+// internal.h -- library-private types of libllrl (host C++ + CUDA).
+// Nothing here is shared with oracle/ (independent paths).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "llrl.h"
+
+namespace llrl {
+
+constexpr int kMaxRanks = 64;      // per side; kernel parameter tables are sized by it
+constexpr int kMaxDevices = 16;
+constexpr int64_t kAlign = 256;    // R0: every piece starts at a 256-byte boundary
+constexpr int kFp8Block = 128;     // R7
+
+void set_error(const char *fmt, ...);
+int64_t dtype_bytes(int dt);
+
+// A rectangle [r0, r1) x [c0, c1) of a full parameter tensor.
+struct Rect {
+    int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+    int64_t rows() const { return r1 - r0; }
+    int64_t cols() const { return c1 - c0; }
+    int64_t area() const { return rows() * cols(); }
+    bool empty() const { return r1 <= r0 || c1 <= c0; }
+    bool operator==(const Rect &o) const { return r0 == o.r0 && r1 == o.r1 && c0 == o.c0 && c1 == o.c1; }
+};
+inline Rect intersect(const Rect &a, const Rect &b) {
+    Rect r{std::max(a.r0, b.r0), std::min(a.r1, b.r1), std::max(a.c0, b.c0), std::min(a.c1, b.c1)};
+    if (r.empty()) r = Rect{};
+    return r;
+}
+
+// Full (unsharded) source parameter.
+struct SrcParam {
+    int kind;      // LLRL_P_*
+    int layer;
+    int64_t rows, cols;
+    int split;     // 0 = rows (column-parallel), 1 = cols (row-parallel), 2 = replicated (norm)
+    bool is_norm;
+};
+
+// One contribution of a source parameter to a generator tensor:
+// full rows [fr0, fr0+nr) x cols [fc0, fc0+nc) land at local rows [lr0, ...), cols [0, nc).
+struct DstPart {
+    int src_param;
+    int64_t fr0, fc0, nr, nc, lr0;
+};
+
+struct Piece {          // one parameter on one rank
+    int param;          // index in this side's param list
+    Rect rect;          // src side: rectangle of the full tensor; dst side: local [0,R)x[0,C)
+    int64_t rows, cols; // local shape
+    int64_t byte_off;
+    int64_t scale_off = -1;
+    bool quantised = false;
+    int dtype;
+    std::vector<DstPart> parts;   // dst side only
+};
+
+struct DstParamDesc {
+    int kind, layer;
+    bool quantisable;   // linear weight (qkv / o / gate_up / down)
+};
+
+}  // namespace llrl
+
+struct llrl_layout {
+    bool is_src;
+    llrl_model model;
+    int fsdp, tp_train, tp_gen;
+    int dtype;          // src: data dtype; dst: target dtype (F32/BF16/FP8)
+    uint32_t flags;
+    int n_ranks;
+    std::vector<llrl::SrcParam> src_params;      // canonical source params (both sides keep it)
+    std::vector<llrl::DstParamDesc> dst_params;  // dst side only
+    std::vector<std::vector<llrl::Piece>> pieces;   // [rank][param]
+    std::vector<int64_t> rank_bytes;
+};
+
+namespace llrl {
+// layout.cpp
+std::vector<SrcParam> enumerate_src_params(const llrl_model &m);
+}
+
+// ---- plan ----------------------------------------------------------------
+
+namespace llrl {
+
+enum ItemKind : uint16_t {
+    K_CAST = 0,        // 2-D (or 1-D when rows == 1) relayout + cast to bf16 / copy to f32
+    K_FP8 = 1,         // one 128x128 (or edge) fp8 block, single source
+    K_FP8_MULTI = 2,   // one fp8 block gathered from several sources (pull, R8)
+};
+enum ItemFlag : uint16_t {
+    F_VEC = 1,         // 16-byte vector path legal (offsets / lds / cols aligned)
+    F_DST_F32 = 2,     // destination dtype f32 (identity), else bf16 (K_CAST)
+};
+
+// Device work item (48 bytes).  Offsets in elements of each side's dtype, except
+// fp8 items: dst_off = byte offset of the block's top-left code, aux = byte
+// offset of its scale.  K_FP8_MULTI: src_off = first segment index, src_rank =
+// segment count.
+struct alignas(16) Item {
+    int64_t src_off;
+    int64_t dst_off;
+    int64_t aux;
+    int32_t rows, cols;
+    int32_t src_ld, dst_ld;
+    uint16_t src_rank, dst_rank;
+    uint16_t kind, flags;
+};
+static_assert(sizeof(Item) == 48, "Item layout");
+
+// Segment of a multi-source fp8 block (block-local rectangle + its source).
+struct alignas(16) Seg {
+    int64_t src_off;
+    int32_t src_ld;
+    int32_t src_rank;
+    int32_t r0, c0, rows, cols;
+};
+static_assert(sizeof(Seg) == 32, "Seg layout");
+
+// Host-side tile: one rectangle intersection (param part, src rank, dst rank).
+struct Tile {
+    int src_param;
+    int dst_param;
+    int src_rank, dst_rank;
+    int64_t rows, cols;
+    int64_t src_off, src_ld;   // elements
+    int64_t dst_off, dst_ld;   // elements (fp8: bytes)
+    int64_t lr0, lc0;          // top-left in the generator-local tensor
+    bool quant;
+};
+
+struct DeviceWork {
+    std::vector<Item> items;
+    std::vector<Seg> segs;
+    std::vector<int> signal_devices;   // devices this device writes into (excl. itself)
+    int n_senders_in = 0;              // other devices writing into this device
+    int64_t hbm_read = 0, hbm_write = 0, nvl_tx = 0, nvl_rx = 0;
+    // device-side state (lazily created by the runtime)
+    int uploaded_device = -1;
+    Item *d_items = nullptr;
+    Seg *d_segs = nullptr;
+    unsigned long long *d_done = nullptr;   // last-CTA counter
+    uint64_t epoch = 0;
+    int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
+    int grid_cast = 0, grid_fp8 = 0;
+};
+
+}  // namespace llrl
+
+struct llrl_plan {
+    int n_src, n_dst, n_devices;
+    int src_dtype, dst_dtype;
+    std::vector<int> src_device, dst_device;
+    std::vector<int64_t> src_rank_bytes, dst_rank_bytes;
+    std::vector<llrl::Tile> tiles;
+    std::vector<llrl::DeviceWork> dev;   // indexed by device ordinal
+    std::vector<int64_t> traffic;        // G x G
+    llrl_plan_stats stats;
+    ~llrl_plan();
+};
+
+struct llrl_comm {
+    int device;
+    unsigned long long *flags = nullptr;   // [0]: arrivals into this device
+    unsigned long long *peer_flags[llrl::kMaxDevices] = {};
+    uint64_t expected = 0;                 // cumulative arrivals this device waits for
+    bool ipc_opened[llrl::kMaxDevices] = {};
+};

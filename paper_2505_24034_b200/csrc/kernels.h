@@ -1,0 +1,38 @@
+// kernels.h -- launch interface between the runtime (runtime.cu) and the
+// sm_100a kernels (kernels.cu, init.cu).  Library-private.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace llrl {
+
+// Kernel parameters, passed by value (__grid_constant__): no per-step host->device
+// copy of the pointer tables.
+struct KParams {
+    const Item *items;
+    const Seg *segs;
+    unsigned long long *done;          // per (plan, device) CTA completion counter, or null
+    unsigned long long done_target;    // epoch * gridDim.x of the signalling launch
+    int item_begin, item_end;          // [begin, end) of this launch
+    int n_signal;
+    unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
+    const void *src[kMaxRanks];
+    void *dst[kMaxRanks];
+};
+
+cudaError_t launch_sync(const KParams &P, int mode, bool src_f32, int grid, cudaStream_t stream);
+cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream);
+cudaError_t sync_occupancy(int mode, bool src_f32, int *blocks_per_sm);
+int sync_threads();
+
+// K0 (init.cu): synthetic trainer weights of one piece.
+struct FillPiece {
+    int64_t byte_off, rows, cols, r0, c0;
+    int param, is_norm;
+};
+cudaError_t launch_fill(void *base, const FillPiece *pieces_dev, int n_pieces, int64_t max_elems, bool f32,
+                        uint64_t seed, cudaStream_t stream);
+
+}  // namespace llrl

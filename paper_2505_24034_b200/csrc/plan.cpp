@@ -1,0 +1,401 @@
+// plan.cpp -- step a2: the routing plan.
+//
+// "Re-sharding ... computed by byte-range intersection", made
+// 2-D: every generator part (a rectangle of a full source tensor, R4) is
+// intersected with every trainer piece (R1-R3) holding that tensor.  Each
+// non-empty intersection is a tile (param, src rank, dst rank, rows x cols,
+// src/dst offsets and leading dimensions).  Replicated trainer pieces (norms
+// under trainer TP) contribute one tile from one chosen holder (R5).  Tiles
+// become device work items:
+//   - bf16 / f32 destinations: K_CAST items of <= kChunk elements, executed by
+//     the SOURCE GPU (push: cast before the transfer, so NVLink carries the
+//     destination width);
+//   - fp8 destinations: one item per 128x128 block of the generator-local
+//     tensor (R7); single-source blocks are pushed (K_FP8 on the source GPU),
+//     multi-source blocks are pulled (K_FP8_MULTI on the destination GPU, R8).
+// Each device's items are interleaved across destination devices in
+// proportion to their bytes so that every NVLink peer and the local HBM copy
+// progress together.  The plan also records the traffic matrix and the
+// algorithmic HBM / NVLink bytes that bench.py's roofline uses.
+#include <cstring>
+#include <new>
+#include <numeric>
+
+#include "internal.h"
+
+using namespace llrl;
+
+namespace {
+
+constexpr int64_t kChunk = 128 * 1024;   // elements per K_CAST item (256 KiB of bf16)
+
+struct Builder {
+    const llrl_layout *S, *D;
+    llrl_plan *P;
+    int64_t es_src, es_dst;
+
+    int holder(const std::vector<int> &members, int g) const {
+        for (int r : members)
+            if (P->src_device[r] == P->dst_device[g]) return r;   // same GPU first (R5)
+        return members[size_t(g) % members.size()];              // else rotate by dst rank
+    }
+
+    llrl_status make_tiles() {
+        const int nsrc = S->n_ranks;
+        for (int g = 0; g < D->n_ranks; g++) {
+            for (const Piece &pc : D->pieces[g]) {
+                const int64_t es_d = dtype_bytes(pc.dtype);
+                for (const DstPart &part : pc.parts) {
+                    const Rect F{part.fr0, part.fr0 + part.nr, part.fc0, part.fc0 + part.nc};
+                    // group trainer pieces with identical rectangles (replicas)
+                    std::vector<Rect> rects;
+                    std::vector<std::vector<int>> members;
+                    for (int s = 0; s < nsrc; s++) {
+                        const Rect &r = S->pieces[s][part.src_param].rect;
+                        if (intersect(r, F).empty()) continue;
+                        size_t k = 0;
+                        while (k < rects.size() && !(rects[k] == r)) k++;
+                        if (k == rects.size()) { rects.push_back(r); members.push_back({}); }
+                        members[k].push_back(s);
+                    }
+                    int64_t covered = 0;
+                    for (size_t a = 0; a < rects.size(); a++) {
+                        covered += intersect(rects[a], F).area();
+                        for (size_t b = a + 1; b < rects.size(); b++)
+                            if (!intersect(rects[a], rects[b]).empty()) {
+                                set_error("trainer pieces of param %d overlap without being replicas", part.src_param);
+                                return LLRL_E_INVALID;
+                            }
+                    }
+                    if (covered != F.area()) {
+                        set_error("param %d: trainer shards cover %lld of %lld elements", part.src_param,
+                                  (long long)covered, (long long)F.area());
+                        return LLRL_E_INVALID;
+                    }
+                    for (size_t a = 0; a < rects.size(); a++) {
+                        const int h = holder(members[a], g);
+                        const Piece &sp = S->pieces[h][part.src_param];
+                        const Rect I = intersect(rects[a], F);
+                        Tile t;
+                        t.src_param = part.src_param;
+                        t.dst_param = pc.param;
+                        t.src_rank = h;
+                        t.dst_rank = g;
+                        t.rows = I.rows();
+                        t.cols = I.cols();
+                        t.src_ld = sp.cols;
+                        t.src_off = sp.byte_off / es_src + (I.r0 - sp.rect.r0) * sp.cols + (I.c0 - sp.rect.c0);
+                        t.lr0 = part.lr0 + (I.r0 - F.r0);
+                        t.lc0 = I.c0 - F.c0;
+                        t.dst_ld = pc.cols;
+                        t.dst_off = pc.byte_off / es_d + t.lr0 * pc.cols + t.lc0;
+                        t.quant = pc.quantised;
+                        P->tiles.push_back(t);
+                    }
+                }
+            }
+        }
+        return LLRL_OK;
+    }
+
+    void add_cast_items(const Tile &t, std::vector<Item> &out) {
+        Item base{};
+        base.kind = K_CAST;
+        base.src_rank = uint16_t(t.src_rank);
+        base.dst_rank = uint16_t(t.dst_rank);
+        const uint16_t fl = D->dtype == LLRL_F32 ? F_DST_F32 : 0;
+        const bool contiguous = t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld);
+        if (contiguous) {
+            // one 1-D run: scalar head up to a 16-byte destination boundary, vector body, scalar tail
+            int64_t n = t.rows * t.cols, so = t.src_off, dof = t.dst_off;
+            auto emit = [&](int64_t s, int64_t d, int64_t len, bool vec) {
+                for (int64_t i = 0; i < len; i += kChunk) {
+                    Item it = base;
+                    it.src_off = s + i; it.dst_off = d + i;
+                    it.rows = 1; it.cols = int32_t(std::min(kChunk, len - i));
+                    it.src_ld = it.cols; it.dst_ld = it.cols;
+                    it.flags = uint16_t(fl | (vec ? F_VEC : 0));
+                    out.push_back(it);
+                }
+            };
+            if ((so & 7) == (dof & 7)) {
+                int64_t head = std::min<int64_t>((8 - (dof & 7)) & 7, n);
+                int64_t body = (n - head) / 8 * 8;
+                int64_t tail = n - head - body;
+                if (head) emit(so, dof, head, false);
+                if (body) emit(so + head, dof + head, body, true);
+                if (tail) emit(so + head + body, dof + head + body, tail, false);
+            } else {
+                emit(so, dof, n, false);
+            }
+            return;
+        }
+        const bool vec = (t.src_off % 8 == 0) && (t.dst_off % 8 == 0) && (t.cols % 8 == 0) &&
+                         (t.src_ld % 8 == 0) && (t.dst_ld % 8 == 0);
+        const int64_t rows_per = std::max<int64_t>(1, kChunk / t.cols);
+        for (int64_t r = 0; r < t.rows; r += rows_per) {
+            Item it = base;
+            it.rows = int32_t(std::min(rows_per, t.rows - r));
+            it.cols = int32_t(t.cols);
+            it.src_ld = int32_t(t.src_ld);
+            it.dst_ld = int32_t(t.dst_ld);
+            it.src_off = t.src_off + r * t.src_ld;
+            it.dst_off = t.dst_off + r * t.dst_ld;
+            it.flags = uint16_t(fl | (vec ? F_VEC : 0));
+            out.push_back(it);
+        }
+    }
+
+    // work lists per executing device, per destination device (for interleaving)
+    std::vector<std::vector<std::vector<Item>>> lists;   // [exec dev][dst dev]
+    std::vector<std::vector<std::vector<Seg>>> seglists;
+
+    void account(int exec, int sdev, int ddev, int64_t src_bytes, int64_t dst_bytes, bool pull) {
+        const int G = P->n_devices;
+        P->dev[sdev].hbm_read += src_bytes;
+        P->dev[ddev].hbm_write += dst_bytes;
+        const int64_t wire = pull ? src_bytes : dst_bytes;
+        if (sdev != ddev) {
+            P->dev[sdev].nvl_tx += wire;
+            P->dev[ddev].nvl_rx += wire;
+        }
+        if (pull) P->traffic[size_t(sdev) * G + ddev] += src_bytes;   // read by ddev from sdev
+        else P->traffic[size_t(exec) * G + ddev] += dst_bytes;
+        P->stats.src_bytes += src_bytes;
+        P->stats.dst_bytes += dst_bytes;
+        (void)exec;
+    }
+
+    llrl_status make_items() {
+        const int G = P->n_devices;
+        lists.assign(G, std::vector<std::vector<Item>>(G));
+        seglists.assign(G, std::vector<std::vector<Seg>>(G));
+        // bf16 / f32 tiles
+        for (const Tile &t : P->tiles) {
+            if (t.quant) continue;
+            const int sd = P->src_device[t.src_rank], dd = P->dst_device[t.dst_rank];
+            add_cast_items(t, lists[sd][dd]);
+            account(sd, sd, dd, t.rows * t.cols * es_src, t.rows * t.cols * es_dst, false);
+        }
+        // fp8 blocks: group quantised tiles by (dst rank, dst param)
+        std::map<std::pair<int, int>, std::vector<size_t>> by_param;
+        for (size_t i = 0; i < P->tiles.size(); i++)
+            if (P->tiles[i].quant) by_param[{P->tiles[i].dst_rank, P->tiles[i].dst_param}].push_back(i);
+        for (auto &kv : by_param) {
+            const int g = kv.first.first;
+            const Piece &pc = D->pieces[g][kv.first.second];
+            const int dd = P->dst_device[g];
+            const int64_t nbr = (pc.rows + kFp8Block - 1) / kFp8Block, nbc = (pc.cols + kFp8Block - 1) / kFp8Block;
+            for (int64_t bi = 0; bi < nbr; bi++)
+                for (int64_t bj = 0; bj < nbc; bj++) {
+                    const Rect B{bi * kFp8Block, std::min(pc.rows, (bi + 1) * kFp8Block),
+                                 bj * kFp8Block, std::min(pc.cols, (bj + 1) * kFp8Block)};
+                    std::vector<std::pair<size_t, Rect>> segs;
+                    for (size_t ti : kv.second) {
+                        const Tile &t = P->tiles[ti];
+                        const Rect I = intersect(Rect{t.lr0, t.lr0 + t.rows, t.lc0, t.lc0 + t.cols}, B);
+                        if (!I.empty()) segs.push_back({ti, I});
+                    }
+                    Item it{};
+                    it.dst_rank = uint16_t(g);
+                    it.rows = int32_t(B.rows());
+                    it.cols = int32_t(B.cols());
+                    it.dst_off = pc.byte_off + B.r0 * pc.cols + B.c0;
+                    it.dst_ld = int32_t(pc.cols);
+                    it.aux = pc.scale_off + (bi * nbc + bj) * 4;
+                    P->stats.n_fp8_blocks++;
+                    if (segs.size() == 1 && segs[0].second == B) {
+                        const Tile &t = P->tiles[segs[0].first];
+                        const int sd = P->src_device[t.src_rank];
+                        it.kind = K_FP8;
+                        it.src_rank = uint16_t(t.src_rank);
+                        it.src_off = t.src_off + (B.r0 - t.lr0) * t.src_ld + (B.c0 - t.lc0);
+                        it.src_ld = int32_t(t.src_ld);
+                        const bool vec = it.cols % 16 == 0 && it.src_off % 8 == 0 && it.src_ld % 8 == 0 &&
+                                         it.dst_off % 16 == 0 && it.dst_ld % 16 == 0;
+                        it.flags = vec ? F_VEC : 0;
+                        lists[sd][dd].push_back(it);
+                        account(sd, sd, dd, B.area() * es_src, B.area() + 4, false);
+                    } else {
+                        it.kind = K_FP8_MULTI;
+                        P->stats.n_fp8_pull_blocks++;
+                        auto &sl = seglists[dd][dd];
+                        it.src_off = int64_t(sl.size());
+                        it.src_rank = uint16_t(segs.size());   // segment count
+                        for (auto &s : segs) {
+                            const Tile &t = P->tiles[s.first];
+                            const Rect &I = s.second;
+                            Seg sg{};
+                            sg.src_rank = t.src_rank;
+                            sg.src_ld = int32_t(t.src_ld);
+                            sg.src_off = t.src_off + (I.r0 - t.lr0) * t.src_ld + (I.c0 - t.lc0);
+                            sg.r0 = int32_t(I.r0 - B.r0);
+                            sg.c0 = int32_t(I.c0 - B.c0);
+                            sg.rows = int32_t(I.rows());
+                            sg.cols = int32_t(I.cols());
+                            sl.push_back(sg);
+                            account(dd, P->src_device[t.src_rank], dd, I.area() * es_src, 0, true);
+                        }
+                        account(dd, dd, dd, 0, B.area() + 4, false);
+                        P->stats.src_bytes += 0;
+                        lists[dd][dd].push_back(it);
+                    }
+                }
+        }
+        // interleave per executing device by fractional progress through each destination list
+        for (int e = 0; e < G; e++) {
+            DeviceWork &W = P->dev[e];
+            // segments: only pull items (dst == exec) use them
+            W.segs = std::move(seglists[e][e]);
+            struct Cursor { int dst; size_t pos; double total, done; };
+            std::vector<Cursor> cur;
+            auto item_bytes = [](const Item &it) { return double(it.rows) * double(it.cols); };
+            for (int d = 0; d < G; d++) {
+                if (lists[e][d].empty()) continue;
+                double tot = 0;
+                for (auto &it : lists[e][d]) tot += item_bytes(it);
+                // rotate the start by the executing device so senders spread over receivers
+                cur.push_back({d, 0, tot, 0});
+                if (d != e) W.signal_devices.push_back(d);
+            }
+            std::rotate(cur.begin(), cur.begin() + (cur.empty() ? 0 : size_t(e) % cur.size()), cur.end());
+            size_t n_total = 0;
+            for (auto &c : cur) n_total += lists[e][c.dst].size();
+            W.items.reserve(n_total);
+            while (W.items.size() < n_total) {
+                Cursor *best = nullptr;
+                double best_frac = 2.0;
+                for (auto &c : cur) {
+                    if (c.pos >= lists[e][c.dst].size()) continue;
+                    const double f = c.done / c.total;
+                    if (f < best_frac) { best_frac = f; best = &c; }
+                }
+                const Item &it = lists[e][best->dst][best->pos++];
+                best->done += item_bytes(it);
+                W.items.push_back(it);
+            }
+            // [cast items | fp8 items]: one launch per class (different register budgets)
+            auto mid = std::stable_partition(W.items.begin(), W.items.end(),
+                                             [](const Item &it) { return it.kind == K_CAST; });
+            W.n_cast = int64_t(mid - W.items.begin());
+            P->stats.n_items += int64_t(W.items.size());
+        }
+        for (int e = 0; e < G; e++)
+            for (int d : P->dev[e].signal_devices) P->dev[d].n_senders_in++;
+        return LLRL_OK;
+    }
+};
+
+bool same_model(const llrl_model &a, const llrl_model &b) { return std::memcmp(&a, &b, sizeof a) == 0; }
+
+}  // namespace
+
+llrl_plan::~llrl_plan() = default;   // device tables are released by llrl_plan_destroy (runtime.cu)
+
+extern "C" {
+
+llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, const int *src_device,
+                             const int *dst_device, uint32_t flags, llrl_plan **out) {
+    (void)flags;
+    if (!src || !dst || !src_device || !dst_device || !out || !src->is_src || dst->is_src) {
+        set_error("llrl_plan_create: invalid argument");
+        return LLRL_E_INVALID;
+    }
+    if (!same_model(src->model, dst->model) || src->src_params.size() != dst->src_params.size()) {
+        set_error("llrl_plan_create: src and dst describe different models");
+        return LLRL_E_MISMATCH;
+    }
+    llrl_plan *P = new (std::nothrow) llrl_plan();
+    if (!P) { set_error("out of host memory"); return LLRL_E_NOMEM; }
+    P->n_src = src->n_ranks;
+    P->n_dst = dst->n_ranks;
+    P->src_dtype = src->dtype;
+    P->dst_dtype = dst->dtype;
+    P->src_device.assign(src_device, src_device + P->n_src);
+    P->dst_device.assign(dst_device, dst_device + P->n_dst);
+    P->src_rank_bytes = src->rank_bytes;
+    P->dst_rank_bytes = dst->rank_bytes;
+    int maxdev = 0;
+    for (int d : P->src_device) maxdev = std::max(maxdev, d);
+    for (int d : P->dst_device) maxdev = std::max(maxdev, d);
+    for (int d : P->src_device) if (d < 0) maxdev = kMaxDevices;
+    for (int d : P->dst_device) if (d < 0) maxdev = kMaxDevices;
+    if (maxdev >= kMaxDevices) {
+        delete P;
+        set_error("llrl_plan_create: device ordinals must be in [0, %d)", kMaxDevices);
+        return LLRL_E_INVALID;
+    }
+    P->n_devices = maxdev + 1;
+    P->dev.resize(P->n_devices);
+    P->traffic.assign(size_t(P->n_devices) * P->n_devices, 0);
+    std::memset(&P->stats, 0, sizeof P->stats);
+    Builder b{src, dst, P, dtype_bytes(src->dtype), dtype_bytes(dst->dtype == LLRL_FP8_E4M3 ? LLRL_BF16 : dst->dtype)};
+    llrl_status st = b.make_tiles();
+    if (st == LLRL_OK) st = b.make_items();
+    if (st != LLRL_OK) { delete P; return st; }
+    P->stats.n_devices = P->n_devices;
+    P->stats.n_src_ranks = P->n_src;
+    P->stats.n_dst_ranks = P->n_dst;
+    P->stats.n_tiles = int64_t(P->tiles.size());
+    *out = P;
+    return LLRL_OK;
+}
+
+static int64_t tile_runs(const Tile &t) {
+    return (t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld)) ? 1 : t.rows;
+}
+
+llrl_status llrl_plan_num_runs(const llrl_plan *p, int64_t *n) {
+    if (!p || !n) { set_error("NULL argument"); return LLRL_E_INVALID; }
+    int64_t s = 0;
+    for (const Tile &t : p->tiles) s += tile_runs(t);
+    *n = s;
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_get_runs(const llrl_plan *p, int64_t first, int64_t count, llrl_run *out) {
+    if (!p || (!out && count) || first < 0 || count < 0) { set_error("invalid argument"); return LLRL_E_INVALID; }
+    int64_t idx = 0, w = 0;
+    for (const Tile &t : p->tiles) {
+        const int64_t nr = tile_runs(t);
+        if (idx + nr <= first) { idx += nr; continue; }
+        for (int64_t k = std::max<int64_t>(0, first - idx); k < nr && w < count; k++) {
+            llrl_run &r = out[w++];
+            r.src_param = t.src_param;
+            r.src_rank = t.src_rank;
+            r.dst_rank = t.dst_rank;
+            r.flags = t.quant ? 1 : 0;
+            if (nr == 1) { r.src_off = t.src_off; r.dst_off = t.dst_off; r.len = t.rows * t.cols; }
+            else { r.src_off = t.src_off + k * t.src_ld; r.dst_off = t.dst_off + k * t.dst_ld; r.len = t.cols; }
+        }
+        idx += nr;
+        if (w == count) break;
+    }
+    if (w != count) { set_error("run range out of bounds"); return LLRL_E_INVALID; }
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_stats_get(const llrl_plan *p, llrl_plan_stats *out) {
+    if (!p || !out) { set_error("NULL argument"); return LLRL_E_INVALID; }
+    *out = p->stats;
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_traffic(const llrl_plan *p, int64_t *bytes) {
+    if (!p || !bytes) { set_error("NULL argument"); return LLRL_E_INVALID; }
+    std::copy(p->traffic.begin(), p->traffic.end(), bytes);
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_device_bytes(const llrl_plan *p, int device, int64_t *hbm_read, int64_t *hbm_write,
+                                   int64_t *nvl_tx, int64_t *nvl_rx) {
+    if (!p || device < 0 || device >= p->n_devices) { set_error("invalid device"); return LLRL_E_INVALID; }
+    const DeviceWork &W = p->dev[device];
+    if (hbm_read) *hbm_read = W.hbm_read;
+    if (hbm_write) *hbm_write = W.hbm_write;
+    if (nvl_tx) *nvl_tx = W.nvl_tx;
+    if (nvl_rx) *nvl_rx = W.nvl_rx;
+    return LLRL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+"""Torch plumbing around libllrl: device buffers, streams, process groups and
+the IPC exchange that maps peer buffers for the push kernels.
+
+One process per GPU (torch.distributed, one rank per device on one node), or a
+single process driving device 0 when every logical trainer/generator rank is
+placed on one GPU.  Every byte of the sync itself is moved by libllrl's
+kernels; this module only allocates, maps and calls.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import llrl
+from synth import MODELS, CONFIGS, LayoutConfig, placement
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+@dataclass
+class JobSpec:
+    cfg: LayoutConfig
+    n_gpus: int
+    n_layers: int | None = None       # override (e.g. a layer slice that fits one GPU)
+    with_embed: int | None = None
+
+    def model(self):
+        m = MODELS[self.cfg.model]
+        kw = {}
+        if self.n_layers is not None:
+            kw["n_layers"] = self.n_layers
+        if self.with_embed is not None:
+            kw["with_embed"] = self.with_embed
+        return m.replace(**kw) if kw else m
+
+
+class SyncJob:
+    """One trainer->generator layout pair placed on `n_gpus` GPUs.
+
+    In a torch.distributed job the calling process owns device ``rank``; without
+    one, the job must fit one device (n_gpus == 1)."""
+
+    def __init__(self, spec: JobSpec, device: int | None = None, seed: int = 0, fill: bool = True):
+        self.spec = spec
+        self.cfg = cfg = spec.cfg
+        self.model = spec.model()
+        d = _dist()
+        self.world = d.get_world_size() if d else 1
+        self.rank = d.get_rank() if d else 0
+        if self.world > 1:
+            assert self.world == spec.n_gpus, "one process per GPU"
+        else:
+            assert spec.n_gpus == 1, "multi-GPU jobs run one process per GPU (torchrun)"
+        self.device = self.rank if device is None else device
+        torch.cuda.set_device(self.device)
+        self.S, self.D = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype,
+                                       cfg.dst_dtype, cfg.fsdp_inner)
+        self.src_dev, self.dst_dev = placement(cfg, spec.n_gpus)
+        self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev)
+        dev = torch.device("cuda", self.device)
+        self.src = {r: torch.empty(self.S.rank_bytes(r), dtype=torch.uint8, device=dev)
+                    for r in range(self.S.n_ranks) if self.src_dev[r] == self.device}
+        self.dst = {g: torch.empty(self.D.rank_bytes(g), dtype=torch.uint8, device=dev)
+                    for g in range(self.D.n_ranks) if self.dst_dev[g] == self.device}
+        self.stream = torch.cuda.current_stream(dev)
+        if fill:
+            self.fill(seed)
+        self.comm = None
+        self._opened = []
+        self.src_ptrs = [self.src[r].data_ptr() if r in self.src else 0 for r in range(self.S.n_ranks)]
+        self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else 0 for g in range(self.D.n_ranks)]
+        if self.world > 1:
+            self._exchange()
+
+    # -- setup ---------------------------------------------------------------
+    def fill(self, seed: int):
+        for r, t in self.src.items():
+            llrl.fill_synthetic(self.S, r, t.data_ptr(), seed, self.stream.cuda_stream)
+        torch.cuda.synchronize(self.device)
+
+    def _exchange(self):
+        """Map every peer's rank buffers and completion flags (cudaIpc over NVLink)."""
+        dist = _dist()
+        self.comm = llrl.Comm(self.device)
+        mine = {"dev": self.device, "flag": self.comm.export(),
+                "src": {r: llrl.ipc_handle(t.data_ptr()) for r, t in self.src.items()},
+                "dst": {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()}}
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine)
+        for h in allh:
+            if h["dev"] == self.device:
+                continue
+            self.comm.import_peer(h["dev"], h["flag"])
+            for r, (hd, off) in h["src"].items():
+                p = llrl.ipc_open(hd, off)
+                self._opened.append((p, off))
+                self.src_ptrs[int(r)] = p
+            for g, (hd, off) in h["dst"].items():
+                p = llrl.ipc_open(hd, off)
+                self._opened.append((p, off))
+                self.dst_ptrs[int(g)] = p
+        dist.barrier()
+
+    # -- the hot path ----------------------------------------------------------
+    def sync(self, stream=None):
+        s = stream if stream is not None else self.stream
+        self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+
+    def sync_host(self, host_src, host_dst, stream=None):
+        """End-to-end entry: host trainer shards in, host generator shards out."""
+        s = stream if stream is not None else self.stream
+        hs = [host_src[r].data_ptr() if r in host_src else 0 for r in range(self.S.n_ranks)]
+        hd = [host_dst[g].data_ptr() if g in host_dst else 0 for g in range(self.D.n_ranks)]
+        self.plan.sync_host(self.comm, self.device, hs, hd, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+
+    def num_launches(self):
+        return self.plan.num_launches(self.device)
+
+    def close(self):
+        for p, off in self._opened:
+            try:
+                llrl.ipc_close(p, off)
+            except llrl.LlrlError:
+                pass
+        self._opened = []
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None
+        self.plan.close()
+
+
+def spec_for(name: str, n_gpus: int) -> JobSpec:
+    """The benchmark job of config `name` at `n_gpus` (SURVEY.md §8(d) placements).
+
+    70B at G=1 does not fit one B200 (282 GB): a 40-layer slice with embed /
+    lm_head is used, as SURVEY §8(d) specifies."""
+    cfg = CONFIGS[name]
+    if cfg.model == "llama3-70b" and n_gpus == 1:
+        return JobSpec(cfg, n_gpus, n_layers=40)
+    return JobSpec(cfg, n_gpus)
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))

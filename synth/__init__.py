@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .configs import MODELS, CONFIGS, Model, LayoutConfig  # noqa: F401
+from .configs import MODELS, CONFIGS, Model, LayoutConfig, placement  # noqa: F401
 
 _M = np.uint64(0xFFFFFFFFFFFFFFFF)
 _K_SEED = np.uint64(0x9E3779B97F4A7C15)

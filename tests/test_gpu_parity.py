@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, bit-exact.
+
+Small sizes (toy, several tiles and ragged tails): every byte of every
+generator buffer.  Full BASELINE sizes, in the launch configuration bench.py
+times (runner.SyncJob, K0-filled inputs): sampled elements and sampled fp8
+blocks computed one by one by the oracle, plus sentinel coverage.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import MODELS, CONFIGS, LayoutConfig
+from tests import harness
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_24034_b200 import build
+    build.build()
+    from paper_2505_24034_b200 import llrl, runner
+    return llrl, runner
+
+
+def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None):
+    llrl, runner = rt
+    cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner)
+    return runner.SyncJob(runner.JobSpec(cfg, 1, n_layers=n_layers), fill=False)
+
+
+def _run_and_compare(rt, job, seed, sentinel=0xA5, inject=None):
+    cfg = job.cfg
+    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
+    src = harness.host_src(ol, seed)
+    if inject is not None:
+        inject(ol, src)
+    for r, t in job.src.items():
+        t.copy_(torch.from_numpy(src[r]))
+    for g, t in job.dst.items():
+        t.fill_(sentinel)
+    job.sync()
+    torch.cuda.synchronize()
+    want = harness.oracle_dst(ol, src, sentinel)
+    for g, t in job.dst.items():
+        got = t.cpu().numpy()
+        if not np.array_equal(got, want[g]):
+            bad = np.nonzero(got != want[g])[0]
+            raise AssertionError(f"dst rank {g}: {bad.size} bytes differ, first at {bad[:8]}")
+
+
+def test_fill_matches_synth(rt):
+    """K0 (CUDA) == synth (numpy) bit for bit: both sides use the same generator."""
+    llrl, runner = rt
+    for sdt in ("f32", "bf16"):
+        job = _toy_job(rt, "toy", 3, 2, 4, sdt, "bf16")
+        job.fill(7)
+        ol = oracle.Layout(job.model, 3, 2, 4, sdt, "bf16")
+        want = harness.host_src(ol, 7)
+        for r, t in job.src.items():
+            assert np.array_equal(t.cpu().numpy(), want[r])
+        job.close()
+
+
+SWEEP = [(f, tt, tg, sdt, ddt) for f in (1, 2, 3, 8) for tt in (1, 2, 4) for tg in (1, 2, 4, 8)
+         for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"))]
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", SWEEP)
+def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
+    job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt)
+    _run_and_compare(rt, job, seed=fsdp * 100 + tpt * 10 + tpg)
+    job.close()
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
+    (2, 1, 2, "f32", "bf16", False),    # C1
+    (3, 1, 4, "f32", "fp8", False),     # multi-source (pull) fp8 blocks
+    (2, 2, 8, "bf16", "fp8", True),     # KV replication + FSDP-inner + multi-source blocks
+    (3, 2, 4, "f32", "f32", False),     # identity (provenance mode)
+    (8, 4, 8, "bf16", "bf16", False),   # 32 trainer ranks
+    (1, 8, 8, "f32", "fp8", False),
+])
+def test_toy_parity_odd(rt, fsdp, tpt, tpg, sdt, ddt, inner):
+    job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, inner)
+    _run_and_compare(rt, job, seed=9)
+    job.close()
+
+
+def _inject_specials(ol, src):
+    """Ties, subnormals, +-0, near-overflow, huge values, fp8 outlier / zero blocks."""
+    rng = np.random.default_rng(3)
+    specials32 = np.array([0x3F808000, 0x3F818000, 0x00038000, 0x80008000, 0x00000001, 0x80000000,
+                           0x00000000, 0x7F7F8000, 0x7F7FFFFF, 0xFF7F0000, 0x3F7FFFFF, 0x0080FFFF,
+                           0x33800000, 0x007FFFFF, 0x477FE000, 0xC3E00000], np.uint32)
+    for r, b in enumerate(src):
+        if ol.src_dtype == "f32":
+            w = b.view(np.uint32)
+            idx = rng.integers(0, w.size, 4096)
+            w[idx] = rng.choice(specials32, idx.size)
+        else:
+            w = b.view(np.uint16)
+            idx = rng.integers(0, w.size, 4096)
+            w[idx] = rng.choice((specials32 >> 16).astype(np.uint16), idx.size)
+        # one all-zero stretch (an fp8 block of zeros when it lands in a linear weight)
+        z = rng.integers(0, max(1, b.size - 70000))
+        b[z:z + 65536] = 0
+
+
+@pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16")])
+def test_toy_parity_special_values(rt, sdt, ddt):
+    job = _toy_job(rt, "toy", 2, 2, 4, sdt, ddt)
+    _run_and_compare(rt, job, seed=5, inject=_inject_specials)
+    job.close()
+
+
+def test_toy_parity_repeated_syncs(rt):
+    """The same plan run many times (epoch counters, no stale state)."""
+    job = _toy_job(rt, "toy", 4, 1, 4, "f32", "bf16")
+    for i in range(5):
+        _run_and_compare(rt, job, seed=20 + i, sentinel=i)
+    job.close()
+
+
+# ---------------------------------------------------------------- full sizes
+
+def _full_job(rt, name, n_layers=None):
+    llrl, runner = rt
+    spec = runner.spec_for(name, 1)
+    if n_layers is not None:
+        spec = runner.JobSpec(spec.cfg, 1, n_layers=n_layers)
+    return runner.SyncJob(spec, seed=0)
+
+
+def _sampled_check(job, n_samples=20000, n_blocks=6, seed=0):
+    cfg = job.cfg
+    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
+    rng = np.random.default_rng(1)
+    for g, t in job.dst.items():
+        n_params = ol.n_dst_params
+        # every generator param: a few elements each; plus the first and last element
+        for gp in range(n_params):
+            R, C, q, off, soff = ol.dst_param(g, gp)
+            if q:
+                continue
+            k = max(2, n_samples // n_params)
+            lr = np.concatenate([[0, R - 1], rng.integers(0, R, k)])
+            lc = np.concatenate([[0, C - 1], rng.integers(0, C, k)])
+            es = 4 if cfg.dst_dtype == "f32" else 2
+            flat = off // es + lr * C + lc
+            dt = torch.int32 if es == 4 else torch.int16
+            got = t.view(dt)[torch.from_numpy(flat).to(t.device)].cpu().numpy()
+            got = got.view(np.uint32 if es == 4 else np.uint16).astype(np.int64)
+            want = harness.expected_elements(ol, 0, g, gp, lr, lc)
+            assert np.array_equal(got, want), (g, gp)
+        if cfg.dst_dtype == "fp8":
+            qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
+            for gp in rng.choice(qparams, n_blocks, replace=False):
+                R, C, q, off, soff = ol.dst_param(g, int(gp))
+                nbr, nbc = -(-R // 128), -(-C // 128)
+                for bi, bj in [(0, 0), (nbr - 1, nbc - 1), (int(rng.integers(nbr)), int(rng.integers(nbc)))]:
+                    qw, sw = harness.expected_fp8_block_fast(ol, 0, g, int(gp), bi, bj)
+                    rows, cols = qw.shape
+                    codes = t[off:off + R * C].view(R, C)[bi * 128:bi * 128 + rows, bj * 128:bj * 128 + cols]
+                    assert np.array_equal(codes.cpu().numpy(), qw), (g, gp, bi, bj)
+                    sc = t[soff + (bi * nbc + bj) * 4:soff + (bi * nbc + bj) * 4 + 4].cpu().numpy().view(np.float32)[0]
+                    assert sc == sw
+
+
+def test_full_c2_8b_sampled(rt):
+    """C2 (Llama-3.1 8B fp32 FSDP=4 -> bf16 TP=4) at G=1, as bench.py runs it."""
+    job = _full_job(rt, "c2")
+    for t in job.dst.values():
+        t.fill_(0xFF)
+    job.sync()
+    torch.cuda.synchronize()
+    # sentinel coverage: no bf16 0xFFFF NaN survives inside any parameter
+    for g, t in job.dst.items():
+        for gp in range(job.D.n_params):
+            v = job.D.param_view(g, gp)
+            seg = t[v.byte_off:v.byte_off + v.rows * v.cols * 2].view(torch.int16)
+            assert not bool((seg == -1).any()), (g, gp)
+    _sampled_check(job)
+    job.close()
+
+
+def test_full_c4_70b_fp8_sampled(rt):
+    """C4 (70B bf16 TP=8 -> fp8 TP=8) at G=1: the 40-layer slice bench.py uses."""
+    job = _full_job(rt, "c4")
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=4000, n_blocks=4)
+    job.close()
+
+
+def test_full_c3_70b_bf16_sampled(rt):
+    """C3 (70B bf16 FSDP=8 -> bf16 TP=8) at G=1, 8-layer slice (memory)."""
+    job = _full_job(rt, "c3", n_layers=8)
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=4000)
+    job.close()

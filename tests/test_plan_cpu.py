@@ -1,0 +1,190 @@
+"""Host logic of the product (no GPU): the C ABI loads and exports every symbol
+include/llrl.h declares; the product's layouts equal the oracle's; the plan's
+canonical runs cover every generator element exactly once and, executed by a
+test-only CPU interpreter, reproduce the oracle's bytes; the plan's traffic
+and byte counts match SURVEY.md App. A / BASELINE.md §3 [derived] figures.
+"""
+from __future__ import annotations
+
+import os
+import re
+
+import ml_dtypes
+import numpy as np
+import pytest
+
+import oracle
+from synth import MODELS, CONFIGS, placement
+from tests import brute
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2505_24034_b200 import build
+    build.build()
+    from paper_2505_24034_b200 import llrl
+    return llrl
+
+
+def test_library_exports_every_declared_symbol(L):
+    hdr = open(os.path.join(ROOT, "include", "llrl.h")).read()
+    declared = set(re.findall(r"^(?:llrl_status|void|const char \*)\s*(llrl_[a-z0-9_]+)\(", hdr, re.M))
+    assert len(declared) >= 25
+    for name in declared:
+        assert hasattr(L.lib(), name), name
+    assert set(L.EXPORTS) == declared
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
+    (f, tt, tg, "f32", "bf16", False) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)
+] + [(2, 2, 8, "bf16", "fp8", True), (3, 1, 4, "f32", "fp8", False), (3, 2, 4, "f32", "f32", False)])
+def test_layout_matches_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner):
+    m = MODELS["toy"]
+    S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, inner)
+    O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, inner)
+    assert S.n_params == O.n_src_params and D.n_params == O.n_dst_params
+    for r in range(S.n_ranks):
+        assert S.rank_bytes(r) == O.src_rank_bytes(r)
+        for p in range(S.n_params):
+            v = S.param_view(r, p)
+            off, r0, r1, c0, c1 = O.src_piece(r, p)
+            assert (v.byte_off, v.full_r0, v.full_r0 + v.rows, v.full_c0, v.full_c0 + v.cols) == (off, r0, r1, c0, c1)
+    for g in range(D.n_ranks):
+        assert D.rank_bytes(g) == O.dst_rank_bytes(g)
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            assert (v.rows, v.cols, v.quantised, v.byte_off, v.scale_off) == O.dst_param(g, gp)
+
+
+def test_layout_errors(L):
+    m = MODELS["toy"]
+    for args, st in [((1, 1, 3), L.E_INDIVISIBLE), ((1, 1, 16), L.E_INDIVISIBLE), ((1, 3, 2), L.E_INDIVISIBLE),
+                     ((0, 1, 2), L.E_INVALID)]:
+        with pytest.raises(L.LlrlError) as e:
+            L.describe(m, *args)
+        assert e.value.status == st
+    with pytest.raises(L.LlrlError) as e:
+        L.describe(m, 1, 1, 2, "bf16", "f32")
+    assert e.value.status == L.E_UNSUPPORTED
+    S, _ = L.describe(m, 2, 1, 2)
+    _, D2 = L.describe(MODELS["toy"].replace(n_layers=1), 2, 1, 2)
+    with pytest.raises(L.LlrlError) as e:
+        L.Plan(S, D2, [0, 0], [0, 0])
+    assert e.value.status == L.E_MISMATCH
+
+
+def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
+    """Test-only CPU interpreter of the plan's canonical runs (not a product path)."""
+    runs = plan.runs()
+    es = {"f32": 4, "bf16": 2}[src_dtype]
+    dst = [np.zeros(n, np.uint8) for n in dst_sizes]
+    # fp8: assemble generator-local fp32 tensors, then quantise per 128x128 block
+    local = {}
+    for r in runs:
+        src = src_bufs[r["src_rank"]]
+        raw = src[r["src_off"] * es:(r["src_off"] + r["len"]) * es]
+        x = raw.view(np.float32) if src_dtype == "f32" else (raw.view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+        g = r["dst_rank"]
+        if r["flags"] & 1:
+            local.setdefault(g, {})
+            buf = local[g].setdefault("codes", np.full(dst_sizes[g], np.nan, np.float32))
+            buf[r["dst_off"]:r["dst_off"] + r["len"]] = x
+        elif dst_dtype == "f32":
+            dst[g][r["dst_off"] * 4:(r["dst_off"] + r["len"]) * 4] = x.view(np.uint8)
+        else:
+            dst[g][r["dst_off"] * 2:(r["dst_off"] + r["len"]) * 2] = x.astype(ml_dtypes.bfloat16).view(np.uint8)
+    for g, d in local.items():
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            if not v.quantised:
+                continue
+            x = d["codes"][v.byte_off:v.byte_off + v.rows * v.cols].reshape(v.rows, v.cols)
+            assert not np.isnan(x).any()
+            q, s = brute.fp8_quant(x)
+            dst[g][v.byte_off:v.byte_off + q.size] = q.reshape(-1)
+            dst[g][v.scale_off:v.scale_off + s.nbytes] = s.view(np.uint8).reshape(-1)
+    return dst
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner,G", [
+    (2, 1, 2, "f32", "bf16", False, 2),
+    (3, 1, 4, "f32", "fp8", False, 2),
+    (2, 2, 8, "bf16", "fp8", True, 4),
+    (3, 2, 4, "f32", "f32", False, 1),
+    (8, 1, 8, "bf16", "bf16", False, 8),
+    (2, 4, 8, "bf16", "bf16", False, 8),
+    (1, 8, 8, "bf16", "fp8", False, 8),
+])
+def test_plan_runs_reproduce_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner, G):
+    m = MODELS["toy"]
+    S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, inner)
+    ns, nd = fsdp * tpt, tpg
+    plan = L.Plan(S, D, [r * G // ns for r in range(ns)], [g * G // nd for g in range(nd)])
+    src, _ = brute.build(m, 4, fsdp, tpt, tpg, sdt, ddt, inner)
+    O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, inner)
+    want = [np.zeros(O.dst_rank_bytes(g), np.uint8) for g in range(nd)]
+    assert O.sync(src, want) == 0
+    got = _interpret(L, plan, D, src, sdt, ddt, [w.size for w in want])
+    for g in range(nd):
+        assert np.array_equal(got[g], want[g]), g
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg", [(f, tt, tg) for f in (1, 3, 8) for tt in (1, 2, 8) for tg in (1, 4, 8)])
+def test_plan_runs_cover_dst_exactly_once(L, fsdp, tpt, tpg):
+    m = MODELS["toy"]
+    S, D = L.describe(m, fsdp, tpt, tpg, "f32", "bf16")
+    plan = L.Plan(S, D, [0] * (fsdp * tpt), [0] * tpg)
+    runs = plan.runs()
+    cover = [np.zeros(D.rank_bytes(g) // 2, np.int32) for g in range(tpg)]
+    for r in runs:
+        cover[r["dst_rank"]][r["dst_off"]:r["dst_off"] + r["len"]] += 1
+    for g in range(tpg):
+        expect = np.zeros_like(cover[g])
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            expect[v.byte_off // 2:v.byte_off // 2 + v.rows * v.cols] = 1
+        assert np.array_equal(cover[g], expect)
+
+
+def _plan_for(L, name, G):
+    cfg = CONFIGS[name]
+    S, D = L.describe(MODELS[cfg.model], cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype,
+                      cfg.fsdp_inner)
+    sd, dd = placement(cfg, G)
+    return L.Plan(S, D, sd, dd)
+
+
+def test_plan_traffic_matches_survey_appendix_a(L):
+    """SURVEY.md App. A "Traffic matrices, G=8 (GB)" [derived] and §8(d) table."""
+    t = np.array(_plan_for(L, "c3", 8).traffic()) / 1e9
+    assert np.allclose(np.diag(t), 12.354, atol=0.002)
+    off = t[~np.eye(8, dtype=bool)]
+    assert np.allclose(off, 0.755, atol=0.002)
+    t = np.array(_plan_for(L, "c2", 8).traffic()) / 1e9
+    for i in range(4):
+        assert abs(t[i, 4 + i] - 3.109) < 0.002
+        for j in range(4, 8):
+            if j != 4 + i:
+                assert abs(t[i, j] - 0.302) < 0.002
+    assert abs(t.sum() - 16.06) < 0.01
+    t = np.array(_plan_for(L, "c5", 8).traffic()) / 1e9
+    for i in range(8):   # "10.47 to one peer and 2.28 to another, diagonal local only for GPUs 0 and 7"
+        row = sorted(t[i], reverse=True)
+        assert abs(row[0] - 10.47) < 0.01 and abs(row[1] - 2.28) < 0.01
+        assert (abs(t[i, i] - 10.47) < 0.01) == (i in (0, 7))
+
+
+def test_plan_bytes_match_baseline_roofline_table(L):
+    """BASELINE.md §3 / SURVEY §8(d): C2 at G=1 moves 48.19 GB through HBM;
+    C3 at G=8: max HBM/GPU 35.28 GB, max egress 5.29 GB."""
+    p = _plan_for(L, "c2", 1)
+    b = p.device_bytes(0)
+    assert abs((b["hbm_read"] + b["hbm_write"]) / 1e9 - 48.19) < 0.01
+    p = _plan_for(L, "c3", 8)
+    hbm = max(p.device_bytes(d)["hbm_read"] + p.device_bytes(d)["hbm_write"] for d in range(8)) / 1e9
+    tx = max(p.device_bytes(d)["nvl_tx"] for d in range(8)) / 1e9
+    assert abs(hbm - 35.28) < 0.01 and abs(tx - 5.29) < 0.01
+    s = _plan_for(L, "c4", 8).stats()
+    assert s.n_fp8_pull_blocks == 0 and s.n_fp8_blocks == 80 * 52224
