@@ -142,6 +142,16 @@ llrl_status llrl_plan_traffic(const llrl_plan *p, int64_t *bytes_GxG);
 llrl_status llrl_plan_device_bytes(const llrl_plan *p, int device, int64_t *hbm_read,
                                    int64_t *hbm_write, int64_t *nvl_tx, int64_t *nvl_rx);
 
+/* Per-device share of one sync. */
+typedef struct {
+    int64_t n_items, n_cast_items, n_fp8_items, n_fp8_pull_items;
+    int32_t n_signal;      /* devices this device writes into (and signals) */
+    int32_t n_senders_in;  /* other devices writing into this device (it waits for them) */
+    int32_t n_launches;    /* kernels llrl_sync enqueues on this device */
+    int32_t reserved;
+} llrl_device_info;
+llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
+
 /* ---- completion comm (a6) --------------------------------------------------
  * A comm owns one 256-byte flag buffer on `device` (epoch counters, R10).
  * Devices that exchange data in a plan must know each other's flag buffers:

@@ -156,6 +156,19 @@ llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n) {
     return LLRL_OK;
 }
 
+llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out) {
+    if (!p || !out || device < 0 || device >= p->n_devices) { set_error("invalid argument"); return LLRL_E_INVALID; }
+    const DeviceWork &W = p->dev[device];
+    std::memset(out, 0, sizeof *out);
+    out->n_items = int64_t(W.items.size());
+    out->n_cast_items = W.n_cast;
+    out->n_fp8_items = out->n_items - W.n_cast;
+    for (const Item &it : W.items) out->n_fp8_pull_items += it.kind == K_FP8_MULTI;
+    out->n_signal = int32_t(W.signal_devices.size());
+    out->n_senders_in = W.n_senders_in;
+    return llrl_sync_num_launches(p, device, &out->n_launches);
+}
+
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void *const *host_src,
                            void *const *host_dst, void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
     if (!p || !host_src || !host_dst || !src_ptrs || !dst_ptrs || device < 0 || device >= p->n_devices) {

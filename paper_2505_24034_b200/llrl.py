@@ -30,7 +30,7 @@ EXPORTS = [
     "llrl_layout_describe", "llrl_layout_num_ranks", "llrl_layout_num_params", "llrl_layout_rank_bytes",
     "llrl_layout_param_view", "llrl_layout_destroy", "llrl_plan_create", "llrl_plan_destroy",
     "llrl_plan_num_runs", "llrl_plan_get_runs", "llrl_plan_stats_get", "llrl_plan_traffic",
-    "llrl_plan_device_bytes", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
+    "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
     "llrl_comm_set_peer", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
     "llrl_sync", "llrl_sync_host", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_last_error",
     "llrl_version",
@@ -67,6 +67,12 @@ class PlanStats(ctypes.Structure):
                 ("n_fp8_pull_blocks", ctypes.c_int64), ("src_bytes", ctypes.c_int64), ("dst_bytes", ctypes.c_int64)]
 
 
+class DeviceInfo(ctypes.Structure):
+    _fields_ = [("n_items", ctypes.c_int64), ("n_cast_items", ctypes.c_int64), ("n_fp8_items", ctypes.c_int64),
+                ("n_fp8_pull_items", ctypes.c_int64), ("n_signal", ctypes.c_int32),
+                ("n_senders_in", ctypes.c_int32), ("n_launches", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 _vp, _i64, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
 _P = ctypes.POINTER
 
@@ -89,6 +95,7 @@ _sig("llrl_plan_get_runs", [_vp, _i64, _i64, _P(Run)])
 _sig("llrl_plan_stats_get", [_vp, _P(PlanStats)])
 _sig("llrl_plan_traffic", [_vp, _P(_i64)])
 _sig("llrl_plan_device_bytes", [_vp, _int, _P(_i64), _P(_i64), _P(_i64), _P(_i64)])
+_sig("llrl_plan_device_info", [_vp, _int, _P(DeviceInfo)])
 _sig("llrl_comm_create", [_int, _P(_vp)])
 _sig("llrl_comm_export", [_vp, ctypes.c_char_p])
 _sig("llrl_comm_import", [_vp, _int, ctypes.c_char_p])
@@ -196,6 +203,11 @@ class Plan:
         v = [_i64() for _ in range(4)]
         _check(_lib.llrl_plan_device_bytes(self._h, device, *[ctypes.byref(x) for x in v]))
         return dict(zip(("hbm_read", "hbm_write", "nvl_tx", "nvl_rx"), (x.value for x in v)))
+
+    def device_info(self, device) -> DeviceInfo:
+        v = DeviceInfo()
+        _check(_lib.llrl_plan_device_info(self._h, device, ctypes.byref(v)))
+        return v
 
     def num_runs(self):
         n = _i64()

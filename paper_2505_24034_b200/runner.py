@@ -87,23 +87,22 @@ class SyncJob:
         """Map every peer's rank buffers and completion flags (cudaIpc over NVLink)."""
         dist = _dist()
         self.comm = llrl.Comm(self.device)
-        mine = {"dev": self.device, "flag": self.comm.export(),
-                "src": {r: llrl.ipc_handle(t.data_ptr()) for r, t in self.src.items()},
-                "dst": {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()}}
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine)
-        for h in allh:
-            if h["dev"] == self.device:
-                continue
-            self.comm.import_peer(h["dev"], h["flag"])
-            for r, (hd, off) in h["src"].items():
-                p = llrl.ipc_open(hd, off)
-                self._opened.append((p, off))
-                self.src_ptrs[int(r)] = p
-            for g, (hd, off) in h["dst"].items():
-                p = llrl.ipc_open(hd, off)
-                self._opened.append((p, off))
-                self.dst_ptrs[int(g)] = p
+        mine = exchange_meta(self.device, self.comm.export(),
+                             {r: llrl.ipc_handle(t.data_ptr()) for r, t in self.src.items()},
+                             {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()})
+        allm = [None] * self.world
+        dist.all_gather_object(allm, mine)
+        opened = {}
+
+        def opener(handle):
+            base = llrl.ipc_open(handle, 0)
+            opened[handle] = base
+            return base
+
+        flags = map_peers(allm, self.device, self.src_ptrs, self.dst_ptrs, opener)
+        for dev, h in flags.items():
+            self.comm.import_peer(dev, h)
+        self._opened = [(b, 0) for b in opened.values()]
         dist.barrier()
 
     # -- the hot path ----------------------------------------------------------
@@ -132,6 +131,31 @@ class SyncJob:
             self.comm.close()
             self.comm = None
         self.plan.close()
+
+
+def exchange_meta(device, flag_handle, src_handles, dst_handles):
+    """What one process publishes: its device, its flag-buffer IPC handle and, per
+    owned rank buffer, (allocation IPC handle, byte offset in the allocation)."""
+    return {"dev": device, "flag": flag_handle, "src": dict(src_handles), "dst": dict(dst_handles)}
+
+
+def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener):
+    """Fill src_ptrs / dst_ptrs (in place) with peer-mapped addresses of every rank
+    buffer other processes own.  Each distinct allocation handle is opened once
+    (several rank buffers may share one caching-allocator segment); returns
+    {peer device: flag handle}.  Pure host logic (tested on gloo, CPU)."""
+    bases = {}
+    flags = {}
+    for m in all_meta:
+        if m["dev"] == my_device:
+            continue
+        flags[m["dev"]] = m["flag"]
+        for table, ptrs in (("src", src_ptrs), ("dst", dst_ptrs)):
+            for r, (h, off) in m[table].items():
+                if h not in bases:
+                    bases[h] = opener(h)
+                ptrs[int(r)] = bases[h] + off
+    return flags
 
 
 def spec_for(name: str, n_gpus: int) -> JobSpec:

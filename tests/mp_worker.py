@@ -1,0 +1,102 @@
+"""Multi-GPU parity worker (one process per GPU), launched by
+tests/test_gpu_multi.py as
+
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+      --master-port P tests/mp_worker.py [--full]
+
+Each rank owns the trainer / generator ranks placed on its GPU, maps its
+peers' buffers over IPC, runs llrl_sync (push over NVLink + completion flags)
+and compares every generator buffer it owns with the CPU oracle, byte for byte
+(toy), or by oracle point checks (full C2 / C3 sizes with --full).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+from synth import LayoutConfig  # noqa: E402
+from tests import harness  # noqa: E402
+
+
+def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2):
+    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner)
+    job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False)
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner)
+    for rep in range(reps):
+        src = harness.host_src(ol, seed + rep)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x5A)
+        torch.cuda.synchronize()
+        dist.barrier()
+        job.sync()
+        torch.cuda.synchronize()
+        dist.barrier()
+        want = harness.oracle_dst(ol, src, 0x5A)
+        for g, t in job.dst.items():
+            got = t.cpu().numpy()
+            if not np.array_equal(got, want[g]):
+                bad = np.nonzero(got != want[g])[0]
+                raise AssertionError(f"{cfg} rep {rep}: dst rank {g} differs at {bad.size} bytes, first {bad[:6]}")
+    job.close()
+
+
+def full_case(runner, world, name):
+    from tests.test_gpu_parity import _sampled_check
+    spec = runner.spec_for(name, world)
+    job = runner.SyncJob(spec, seed=0)
+    for t in job.dst.values():
+        t.fill_(0xFF)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(3):
+        job.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    _sampled_check(job, n_samples=4000, n_blocks=3)
+    job.close()
+
+
+def main():
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_24034_b200 import runner
+    cases = [
+        (2, 1, 2, "f32", "bf16", "disjoint"),
+        (4, 1, 4, "f32", "bf16", "disjoint"),
+        (8, 1, 8, "bf16", "bf16", "colocated"),
+        (2, 4, 8, "bf16", "bf16", "colocated"),
+        (1, 8, 8, "bf16", "fp8", "colocated"),
+        (1, 8, 8, "bf16", "fp8", "rotated"),
+        (3, 1, 4, "f32", "fp8", "colocated"),     # pull (multi-source) fp8 blocks across GPUs
+        (2, 2, 8, "bf16", "fp8", "rotated"),
+        (3, 2, 4, "f32", "f32", "disjoint"),
+    ]
+    for c in cases:
+        toy_case(runner, world, *c)
+        if dist.get_rank() == 0:
+            print("ok", c, flush=True)
+    if "--full" in sys.argv:
+        for name in ("c2", "c3"):
+            full_case(runner, world, name)
+            if dist.get_rank() == 0:
+                print("ok full", name, flush=True)
+    dist.barrier()
+    if dist.get_rank() == 0:
+        print("MP_OK", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
