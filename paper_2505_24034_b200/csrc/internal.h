@@ -152,6 +152,7 @@ struct DeviceWork {
     uint64_t epoch = 0;
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
     int grid_cast = 0, grid_fp8 = 0;
+    int variant = 0;                   // cast-kernel variant (kernels.cu)
 };
 
 }  // namespace llrl

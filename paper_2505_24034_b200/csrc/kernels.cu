@@ -33,6 +33,10 @@ __device__ __forceinline__ uint4 ld_stream(const void *p) {
     return r;
 }
 
+__device__ __forceinline__ void st_v2(void *p, uint32_t x, uint32_t y) {
+    asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(x), "r"(y) : "memory");
+}
+
 __device__ __forceinline__ void st_v4(void *p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
@@ -64,51 +68,48 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 // ---- K1: relayout + cast ----------------------------------------------------
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
 
-// 8 elements (one 16-byte destination vector for bf16) per vector step.
-template <bool SRC_F32>
+// One "unit" = 16 bytes of SOURCE (4 fp32 or 8 bf16 elements).  Thread t of a
+// CTA handles units t, t + 256, ... so every warp-wide load instruction reads
+// 512 contiguous bytes and every store instruction writes 256 (f32->bf16,
+// 8-byte stores) or 512 contiguous bytes: full 32-byte sectors both ways.
+// U units per thread are loaded before any is stored (U x 16 B in flight).
+template <bool SRC_F32, int U>
 __device__ __forceinline__ void cast_item(const Item &it, const KParams &P) {
     const char *src = static_cast<const char *>(P.src[it.src_rank]);
     char *dst = static_cast<char *>(P.dst[it.dst_rank]);
     constexpr int es = SRC_F32 ? 4 : 2;
+    constexpr int E = 16 / es;                       // elements per unit
     const bool dst_f32 = it.flags & F_DST_F32;
-    if (it.flags & F_VEC) {
-        const int vpr = it.cols >> 3;
-        const int nvec = it.rows * vpr;
-        for (int v0 = threadIdx.x; v0 < nvec; v0 += kThreads * kUnroll) {
-            uint4 a[kUnroll], b[kUnroll];
+    if (it.flags & F_VEC) {                          // planner: offsets, lds, cols multiples of 8 elements
+        const int upr = it.cols / E;                 // units per row
+        const int nunits = it.rows * upr;
+        const bool one_d = it.rows == 1;
+        const char *sbase = src + it.src_off * es;
+        char *dbase = dst + it.dst_off * (dst_f32 ? 4 : 2);
+        for (int u0 = threadIdx.x; u0 < nunits; u0 += kThreads * U) {
+            uint4 a[U];
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const int v = v0 + u * kThreads;
-                if (v < nvec) {
-                    const int r = v / vpr, c = (v - r * vpr) << 3;
-                    const char *s = src + (it.src_off + int64_t(r) * it.src_ld + c) * es;
-                    a[u] = ld_stream(s);
-                    if (SRC_F32) b[u] = ld_stream(s + 16);
+            for (int k = 0; k < U; k++) {
+                const int u = u0 + k * kThreads;
+                if (u < nunits) {
+                    int r = 0, c = u * E;
+                    if (!one_d) { r = u / upr; c = (u - r * upr) * E; }
+                    a[k] = ld_stream(sbase + (int64_t(r) * it.src_ld + c) * es);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const int v = v0 + u * kThreads;
-                if (v < nvec) {
-                    const int r = v / vpr, c = (v - r * vpr) << 3;
-                    const int64_t doff = it.dst_off + int64_t(r) * it.dst_ld + c;
-                    if (SRC_F32) {
-                        if (dst_f32) {
-                            st_v4(dst + doff * 4, a[u]);
-                            st_v4(dst + doff * 4 + 16, b[u]);
-                        } else {
-                            uint4 o;
-                            o.x = bf16x2_rn(__uint_as_float(a[u].x), __uint_as_float(a[u].y));
-                            o.y = bf16x2_rn(__uint_as_float(a[u].z), __uint_as_float(a[u].w));
-                            o.z = bf16x2_rn(__uint_as_float(b[u].x), __uint_as_float(b[u].y));
-                            o.w = bf16x2_rn(__uint_as_float(b[u].z), __uint_as_float(b[u].w));
-                            st_v4(dst + doff * 2, o);
-                        }
-                    } else {
-                        st_v4(dst + doff * 2, a[u]);
-                    }
+            for (int k = 0; k < U; k++) {
+                const int u = u0 + k * kThreads;
+                if (u >= nunits) break;
+                int r = 0, c = u * E;
+                if (!one_d) { r = u / upr; c = (u - r * upr) * E; }
+                const int64_t doff = int64_t(r) * it.dst_ld + c;
+                if (SRC_F32 && !dst_f32) {
+                    st_v2(dbase + doff * 2, bf16x2_rn(__uint_as_float(a[k].x), __uint_as_float(a[k].y)),
+                          bf16x2_rn(__uint_as_float(a[k].z), __uint_as_float(a[k].w)));
+                } else {
+                    st_v4(dbase + doff * es, a[k]);   // identity (f32->f32, bf16->bf16)
                 }
             }
         }
@@ -273,37 +274,43 @@ __device__ void fp8_item_generic(const Item &it, const KParams &P, uint32_t *s_r
 
 // ---- the persistent sync kernel + K3 signal -------------------------------------
 
-// MODE 0: relayout + cast items only (low register count -> full occupancy);
-// MODE 1: fp8 block items.  The planner sorts a device's items as
-// [cast items | fp8 items]; each launch covers one contiguous range.
-template <bool SRC_F32, int MODE>
-__global__ void __launch_bounds__(kThreads) llrl_k_sync(const __grid_constant__ KParams P) {
+// Completion (a6): every thread orders its stores at system scope, the CTA
+// joins, one thread counts the CTA in; the last CTA of the launch publishes one
+// arrival to every destination device with a release add at system scope.
+__device__ __forceinline__ void complete(const KParams &P) {
+    if (P.done == nullptr) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long prev = atomicAdd(P.done, 1ULL);
+        if (prev + 1 == P.done_target) {
+            __threadfence_system();
+            for (int s = 0; s < P.n_signal; s++)
+                asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(P.signal[s]) : "memory");
+        }
+    }
+}
+
+// K1 launch: relayout + cast items [item_begin, item_end), persistent CTAs.
+template <bool SRC_F32, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) llrl_k_cast(const __grid_constant__ KParams P) {
+    for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+        const Item it = P.items[i];
+        cast_item<SRC_F32, U>(it, P);
+    }
+    complete(P);
+}
+
+// K2 launch: fp8 block items (single-source vector path, or generic / pull).
+template <bool SRC_F32>
+__global__ void __launch_bounds__(kThreads) llrl_k_fp8(const __grid_constant__ KParams P) {
     __shared__ uint32_t s_red[kThreads / 32];
     for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
         const Item it = P.items[i];
-        if (MODE == 0) {
-            cast_item<SRC_F32>(it, P);
-        } else if (it.kind == K_FP8 && (it.flags & F_VEC)) {
-            fp8_item_vec<SRC_F32>(it, P, s_red);
-        } else {
-            fp8_item_generic<SRC_F32>(it, P, s_red);
-        }
+        if (it.kind == K_FP8 && (it.flags & F_VEC)) fp8_item_vec<SRC_F32>(it, P, s_red);
+        else fp8_item_generic<SRC_F32>(it, P, s_red);
     }
-    if (P.done != nullptr) {
-        // Completion (a6): every thread orders its stores at system scope, the CTA
-        // joins, one thread counts the CTA in; the last CTA of this launch
-        // publishes one arrival to every destination device with a release add.
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned long long prev = atomicAdd(P.done, 1ULL);
-            if (prev + 1 == P.done_target) {
-                __threadfence_system();
-                for (int s = 0; s < P.n_signal; s++)
-                    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(P.signal[s]) : "memory");
-            }
-        }
-    }
+    complete(P);
 }
 
 // K3 receiver: spin (acquire, system scope) until `target` arrivals, bounded by
@@ -326,15 +333,26 @@ __global__ void llrl_k_wait(unsigned long long *flag, unsigned long long target,
 
 }  // namespace
 
-template <int MODE>
-static cudaError_t launch_mode(const KParams &P, bool src_f32, int grid, cudaStream_t stream) {
-    if (src_f32) llrl_k_sync<true, MODE><<<grid, kThreads, 0, stream>>>(P);
-    else llrl_k_sync<false, MODE><<<grid, kThreads, 0, stream>>>(P);
-    return cudaGetLastError();
+// Cast-kernel variants (units in flight per thread, min resident CTAs per SM);
+// LLRL_CAST_VARIANT selects one for tuning, default kDefaultCastVariant.
+struct CastVariant {
+    const void *f32, *bf16;
+};
+#define LLRL_CV(U, M) {(const void *)llrl_k_cast<true, U, M>, (const void *)llrl_k_cast<false, U, M>}
+static const CastVariant kCastVariants[] = {LLRL_CV(4, 1), LLRL_CV(8, 1), LLRL_CV(8, 4), LLRL_CV(4, 8),
+                                            LLRL_CV(16, 1), LLRL_CV(2, 8)};
+#undef LLRL_CV
+constexpr int kNumCastVariants = int(sizeof(kCastVariants) / sizeof(kCastVariants[0]));
+
+static const void *kernel_for(int mode, int variant, bool src_f32) {
+    if (mode == 1) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
+    if (variant < 0 || variant >= kNumCastVariants) variant = kDefaultCastVariant;
+    return src_f32 ? kCastVariants[variant].f32 : kCastVariants[variant].bf16;
 }
 
-cudaError_t launch_sync(const KParams &P, int mode, bool src_f32, int grid, cudaStream_t stream) {
-    return mode == 0 ? launch_mode<0>(P, src_f32, grid, stream) : launch_mode<1>(P, src_f32, grid, stream);
+cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream) {
+    void *args[] = {const_cast<KParams *>(&P)};
+    return cudaLaunchKernel(kernel_for(mode, variant, src_f32), dim3(grid), dim3(kThreads), args, 0, stream);
 }
 
 cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream) {
@@ -344,10 +362,10 @@ cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cud
 
 int sync_threads() { return kThreads; }
 
-cudaError_t sync_occupancy(int mode, bool src_f32, int *blocks_per_sm) {
-    const void *fn = mode == 0 ? (src_f32 ? (const void *)llrl_k_sync<true, 0> : (const void *)llrl_k_sync<false, 0>)
-                               : (src_f32 ? (const void *)llrl_k_sync<true, 1> : (const void *)llrl_k_sync<false, 1>);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kThreads, 0);
+cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kernel_for(mode, variant, src_f32), kThreads, 0);
 }
+
+int num_cast_variants() { return kNumCastVariants; }
 
 }  // namespace llrl

@@ -22,9 +22,11 @@ struct KParams {
     void *dst[kMaxRanks];
 };
 
-cudaError_t launch_sync(const KParams &P, int mode, bool src_f32, int grid, cudaStream_t stream);
+constexpr int kDefaultCastVariant = 1;
+cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
 cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream);
-cudaError_t sync_occupancy(int mode, bool src_f32, int *blocks_per_sm);
+cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm);
+int num_cast_variants();
 int sync_threads();
 
 // K0 (init.cu): synthetic trainer weights of one piece.

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -55,9 +56,12 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const int64_t n_cast = W.n_cast, n_fp8 = int64_t(W.items.size()) - W.n_cast;
+    W.variant = kDefaultCastVariant;
+    if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
+    if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     for (int mode = 0; mode < 2; mode++) {
         int per_sm = 0;
-        CK(sync_occupancy(mode, p->src_dtype == LLRL_F32, &per_sm));
+        CK(sync_occupancy(mode, W.variant, p->src_dtype == LLRL_F32, &per_sm));
         if (per_sm < 1) per_sm = 1;
         const int64_t n = mode == 0 ? n_cast : n_fp8;
         const int g = int(std::min<int64_t>(int64_t(sms) * per_sm, std::max<int64_t>(1, n)));
@@ -139,7 +143,7 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
                 kp.n_signal = int(W.signal_devices.size());
                 for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[W.signal_devices[i]];
             }
-            CK(launch_sync(kp, mode, p->src_dtype == LLRL_F32, grid, s));
+            CK(launch_sync(kp, mode, W.variant, p->src_dtype == LLRL_F32, grid, s));
         }
     }
     if (W.n_senders_in > 0) {

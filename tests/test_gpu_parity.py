@@ -206,3 +206,13 @@ def test_full_c3_70b_bf16_sampled(rt):
     torch.cuda.synchronize()
     _sampled_check(job, n_samples=4000)
     job.close()
+
+
+@pytest.mark.parametrize("variant", range(6))
+def test_toy_parity_cast_variants(rt, variant, monkeypatch):
+    """Every cast-kernel variant (LLRL_CAST_VARIANT tuning knob) is bit-exact."""
+    monkeypatch.setenv("LLRL_CAST_VARIANT", str(variant))
+    for sdt, ddt, f, tt, tg in (("f32", "bf16", 3, 2, 4), ("bf16", "bf16", 8, 1, 8), ("f32", "f32", 2, 1, 2)):
+        job = _toy_job(rt, "toy", f, tt, tg, sdt, ddt)
+        _run_and_compare(rt, job, seed=variant)
+        job.close()
