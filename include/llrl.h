@@ -193,11 +193,24 @@ llrl_status llrl_ipc_close(void *dev_ptr, int64_t offset);
 llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device,
                       void *const *src_ptrs, void *const *dst_ptrs, void *stream);
 
+/* Layer-group streaming (NEXT f3: "stream layer l as soon as the optimizer
+ * updates it"): the plan's work split by layer group -- group 0 = embed (if
+ * any), then one group per decoder layer, then final_norm + lm_head.
+ * llrl_sync_group enqueues exactly the work of one group (push, signal, wait),
+ * so group g can be synced while the trainer still updates later layers.  All
+ * processes must issue the same sequence of llrl_sync / llrl_sync_group calls;
+ * running every group once is equivalent to one llrl_sync. */
+llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n);
+llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group,
+                            void *const *src_ptrs, void *const *dst_ptrs, void *stream);
+
 /* Same as llrl_sync, with the trainer shards hosted on this device first
  * copied from HOST buffers host_src[r] and, after the sync, the generator
  * shards resident on this device copied back to host_dst[g] (entries of ranks
- * on other devices are ignored; host buffers should be pinned).  The copies are
- * pipelined with the kernels in chunks.  Device buffers as in llrl_sync. */
+ * on other devices are ignored; host buffers should be pinned).  Pipelined per
+ * layer group on two library-owned copy streams: H2D of group g+1 and D2H of
+ * group g-1 overlap the kernels of group g.  When `stream` passes the end of
+ * the call, every host_dst byte of this device's generator ranks is written. */
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device,
                            const void *const *host_src, void *const *host_dst,
                            void *const *src_ptrs, void *const *dst_ptrs, void *stream);

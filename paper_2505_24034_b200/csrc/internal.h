@@ -143,16 +143,23 @@ struct DeviceWork {
     std::vector<Seg> segs;
     std::vector<int> signal_devices;   // devices this device writes into (excl. itself)
     int n_senders_in = 0;              // other devices writing into this device
+    // layer groups: items [cast_off[g], cast_off[g+1]) and [fp8_off[g], fp8_off[g+1])
+    std::vector<int64_t> cast_off, fp8_off;
+    std::vector<std::vector<int>> group_signal;   // per group: devices written (excl. itself)
+    std::vector<int> group_senders_in;            // per group: other devices writing here
     int64_t hbm_read = 0, hbm_write = 0, nvl_tx = 0, nvl_rx = 0;
     // device-side state (lazily created by the runtime)
     int uploaded_device = -1;
     Item *d_items = nullptr;
     Seg *d_segs = nullptr;
-    unsigned long long *d_done = nullptr;   // last-CTA counter
-    uint64_t epoch = 0;
+    unsigned long long *d_done = nullptr;   // last-CTA counter (cumulative)
+    uint64_t done_total = 0;                // CTAs of all signalling launches so far
+    void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)
+    std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
     int grid_cast = 0, grid_fp8 = 0;
     int variant = 0;                   // cast-kernel variant (kernels.cu)
+    int fp8_variant = 1;               // 0: register kernel, 1: TMA pipeline
 };
 
 }  // namespace llrl
@@ -162,6 +169,8 @@ struct llrl_plan {
     int src_dtype, dst_dtype;
     std::vector<int> src_device, dst_device;
     std::vector<int64_t> src_rank_bytes, dst_rank_bytes;
+    int n_groups = 0;
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> src_group_range, dst_group_range;   // [rank][group]
     std::vector<llrl::Tile> tiles;
     std::vector<llrl::DeviceWork> dev;   // indexed by device ordinal
     std::vector<int64_t> traffic;        // G x G

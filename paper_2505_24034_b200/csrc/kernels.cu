@@ -132,12 +132,17 @@ __device__ __forceinline__ void cast_item(const Item &it, const KParams &P) {
 
 // ---- K2: fp8 block quantisation (R7) ------------------------------------------
 
+// Named barrier over the 256 threads that process blocks (barrier 1): the TMA
+// producer warp of llrl_k_fp8_tma never joins it.
+__device__ __forceinline__ void workers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 // Block-wide max of non-negative fp32 bit patterns (order-preserving as u32).
+// Callers alternate between two 8-word s_red buffers from item to item, so one
+// barrier per item suffices (a warp can run at most one item ahead).
 __device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t *s_red) {
     v = __reduce_max_sync(0xffffffffu, v);
-    __syncthreads();                       // s_red reuse across items
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
-    __syncthreads();
+    workers_sync();
     uint32_t m = s_red[0];
 #pragma unroll
     for (int w = 1; w < kThreads / 32; w++) m = max(m, s_red[w]);
@@ -150,11 +155,57 @@ __device__ __forceinline__ void fp8_scales(uint32_t amax_bits, float *inv, float
     *scale = __fdiv_rn(amax_c, 448.0f);
 }
 
-// Single-source block, vector path: thread t covers rows (t/8) + 32k, k < 4,
-// columns [(t%8)*16, +16).  Raw source words stay in registers between the
-// amax pass and the quantise pass (one HBM read per element).
+// |x| bit patterns of one 16-byte word of source elements, max-accumulated.
 template <bool SRC_F32>
-__device__ __forceinline__ void fp8_item_vec(const Item &it, const KParams &P, uint32_t *s_red) {
+__device__ __forceinline__ uint32_t word_amax(uint4 w, uint32_t amax) {
+    const uint32_t q[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        if (SRC_F32) {
+            amax = max(amax, q[e] & 0x7FFFFFFFu);
+        } else {
+            amax = max(amax, (q[e] << 16) & 0x7FFFFFFFu);
+            amax = max(amax, q[e] & 0x7FFF0000u);
+        }
+    }
+    return amax;
+}
+
+// 16 source elements (W words) -> 16 e4m3 codes (one 16-byte word).
+template <bool SRC_F32, int W>
+__device__ __forceinline__ uint4 quant16(const uint4 *w, float inv) {
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+        const uint32_t q[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (SRC_F32) {
+                x[4 * j + e] = __uint_as_float(q[e]);
+            } else {
+                x[8 * j + 2 * e] = bf16_lo(q[e]);
+                x[8 * j + 2 * e + 1] = bf16_hi(q[e]);
+            }
+        }
+    }
+    uint32_t ow[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const uint32_t lo = e4m3x2_rn(__fmul_rn(x[4 * i], inv), __fmul_rn(x[4 * i + 1], inv));
+        const uint32_t hi = e4m3x2_rn(__fmul_rn(x[4 * i + 2], inv), __fmul_rn(x[4 * i + 3], inv));
+        ow[i] = lo | (hi << 16);
+    }
+    return make_uint4(ow[0], ow[1], ow[2], ow[3]);
+}
+
+// Single-source block, thread t covers rows (t/8) + 32k, k < 4, columns
+// [(t%8)*16, +16).  Raw source words stay in registers between the amax pass
+// and the quantise pass (one HBM read per element).  FROM_SMEM: the block was
+// staged by TMA into `stage` (row pitch 128 elements); else loaded from HBM.
+template <bool SRC_F32, bool FROM_SMEM>
+__device__ __forceinline__ void fp8_block(const Item &it, const KParams &P, const unsigned char *stage,
+                                          uint32_t *s_red) {
+    constexpr int es = SRC_F32 ? 4 : 2;
     constexpr int W = SRC_F32 ? 4 : 2;           // 16-byte words per 16 elements
     const char *src = static_cast<const char *>(P.src[it.src_rank]);
     char *dst = static_cast<char *>(P.dst[it.dst_rank]);
@@ -167,26 +218,21 @@ __device__ __forceinline__ void fp8_item_vec(const Item &it, const KParams &P, u
     for (int k = 0; k < 4; k++) {
         const int r = rg + 32 * k;
         if (col_ok && r < it.rows) {
-            const char *s = src + (it.src_off + int64_t(r) * it.src_ld + cc) * (SRC_F32 ? 4 : 2);
+            if (FROM_SMEM) {
+                const uint4 *s = reinterpret_cast<const uint4 *>(stage + (r * 128 + cc) * es);
 #pragma unroll
-            for (int j = 0; j < W; j++) w[k][j] = ld_stream(s + 16 * j);
+                for (int j = 0; j < W; j++) w[k][j] = s[j];
+            } else {
+                const char *s = src + (it.src_off + int64_t(r) * it.src_ld + cc) * es;
+#pragma unroll
+                for (int j = 0; j < W; j++) w[k][j] = ld_stream(s + 16 * j);
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < W; j++) w[k][j] = make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int j = 0; j < W; j++) {
-            const uint32_t q[4] = {w[k][j].x, w[k][j].y, w[k][j].z, w[k][j].w};
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                if (SRC_F32) {
-                    amax = max(amax, q[e] & 0x7FFFFFFFu);
-                } else {
-                    amax = max(amax, (q[e] << 16) & 0x7FFFFFFFu);
-                    amax = max(amax, q[e] & 0x7FFF0000u);
-                }
-            }
-        }
+        for (int j = 0; j < W; j++) amax = word_amax<SRC_F32>(w[k][j], amax);
     }
     amax = block_max_u32(amax, s_red);
     float inv, scale;
@@ -194,30 +240,8 @@ __device__ __forceinline__ void fp8_item_vec(const Item &it, const KParams &P, u
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         const int r = rg + 32 * k;
-        if (col_ok && r < it.rows) {
-            float x[16];
-#pragma unroll
-            for (int j = 0; j < W; j++) {
-                const uint32_t q[4] = {w[k][j].x, w[k][j].y, w[k][j].z, w[k][j].w};
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    if (SRC_F32) {
-                        x[4 * j + e] = __uint_as_float(q[e]);
-                    } else {
-                        x[8 * j + 2 * e] = bf16_lo(q[e]);
-                        x[8 * j + 2 * e + 1] = bf16_hi(q[e]);
-                    }
-                }
-            }
-            uint32_t ow[4];
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const uint32_t lo = e4m3x2_rn(__fmul_rn(x[4 * i], inv), __fmul_rn(x[4 * i + 1], inv));
-                const uint32_t hi = e4m3x2_rn(__fmul_rn(x[4 * i + 2], inv), __fmul_rn(x[4 * i + 3], inv));
-                ow[i] = lo | (hi << 16);
-            }
-            st_v4(dst + it.dst_off + int64_t(r) * it.dst_ld + cc, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-        }
+        if (col_ok && r < it.rows)
+            st_v4(dst + it.dst_off + int64_t(r) * it.dst_ld + cc, quant16<SRC_F32, W>(w[k], inv));
     }
     if (threadIdx.x == 0) *reinterpret_cast<float *>(dst + it.aux) = scale;
 }
@@ -301,14 +325,111 @@ __global__ void __launch_bounds__(kThreads, MINB) llrl_k_cast(const __grid_const
     complete(P);
 }
 
-// K2 launch: fp8 block items (single-source vector path, or generic / pull).
+// K2 launch, register variant: fp8 block items loaded straight from HBM.
 template <bool SRC_F32>
 __global__ void __launch_bounds__(kThreads) llrl_k_fp8(const __grid_constant__ KParams P) {
-    __shared__ uint32_t s_red[kThreads / 32];
-    for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+    __shared__ uint32_t s_red[2][kThreads / 32];
+    int k = 0;
+    for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x, ++k) {
         const Item it = P.items[i];
-        if (it.kind == K_FP8 && (it.flags & F_VEC)) fp8_item_vec<SRC_F32>(it, P, s_red);
-        else fp8_item_generic<SRC_F32>(it, P, s_red);
+        if (it.kind == K_FP8 && (it.flags & F_VEC)) fp8_block<SRC_F32, false>(it, P, nullptr, s_red[k & 1]);
+        else fp8_item_generic<SRC_F32>(it, P, s_red[k & 1]);
+    }
+    complete(P);
+}
+
+// ---- K2 TMA pipeline -------------------------------------------------------------
+// Warp-specialised: warp 8 (producer) stages each block's rows into shared
+// memory with cp.async.bulk (one bulk copy per row, completion counted in
+// bytes on the stage's mbarrier), up to fp8_stages() blocks ahead; warps 0-7
+// (workers) reduce amax and quantise from shared memory and release the stage.
+// Loads of the next blocks overlap the reduction of the current one.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok)
+                     : "r"(smem_u32(b)), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <bool SRC_F32>
+__host__ __device__ constexpr int fp8_stages() { return SRC_F32 ? 3 : 5; }
+template <bool SRC_F32>
+__host__ __device__ constexpr int fp8_stage_bytes() { return 128 * 128 * (SRC_F32 ? 4 : 2); }
+
+template <bool SRC_F32>
+__global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_fp8_tma(const __grid_constant__ KParams P) {
+    constexpr int S = fp8_stages<SRC_F32>();
+    constexpr int kStage = fp8_stage_bytes<SRC_F32>();
+    constexpr int es = SRC_F32 ? 4 : 2;
+    extern __shared__ __align__(128) unsigned char stages[];
+    __shared__ __align__(8) uint64_t full_bar[S], empty_bar[S];
+    __shared__ Item slot[S];
+    __shared__ uint32_t s_red[2][kThreads / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kThreads / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kThreads / 32) {
+        // producer
+        int k = 0;
+        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x, ++k) {
+            const int st = k % S;
+            mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
+            const Item it = P.items[i];
+            const bool tma = it.kind == K_FP8 && (it.flags & F_VEC);
+            if (lane == 0) {
+                slot[st] = it;
+                if (tma) mbar_arrive_tx(&full_bar[st], uint32_t(it.rows * it.cols * es));
+                else mbar_arrive(&full_bar[st]);
+            }
+            __syncwarp();
+            if (tma) {
+                const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
+                for (int r = lane; r < it.rows; r += 32)
+                    bulk_g2s(stages + st * kStage + r * 128 * es, src + int64_t(r) * it.src_ld * es,
+                             uint32_t(it.cols * es), &full_bar[st]);
+            }
+        }
+    } else {
+        // workers
+        int k = 0;
+        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x, ++k) {
+            const int st = k % S;
+            mbar_wait(&full_bar[st], (k / S) & 1);
+            const Item it = slot[st];
+            if (it.kind == K_FP8 && (it.flags & F_VEC))
+                fp8_block<SRC_F32, true>(it, P, stages + st * kStage, s_red[k & 1]);
+            else
+                fp8_item_generic<SRC_F32>(it, P, s_red[k & 1]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
     }
     complete(P);
 }
@@ -345,14 +466,37 @@ static const CastVariant kCastVariants[] = {LLRL_CV(4, 1), LLRL_CV(8, 1), LLRL_C
 constexpr int kNumCastVariants = int(sizeof(kCastVariants) / sizeof(kCastVariants[0]));
 
 static const void *kernel_for(int mode, int variant, bool src_f32) {
-    if (mode == 1) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
+    if (mode == 1) {
+        if (variant == 0) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
+        return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false>;
+    }
     if (variant < 0 || variant >= kNumCastVariants) variant = kDefaultCastVariant;
     return src_f32 ? kCastVariants[variant].f32 : kCastVariants[variant].bf16;
 }
 
+// Block size and dynamic shared memory of a launch (fp8 TMA: 256 workers + 1 producer warp).
+static void launch_shape(int mode, int variant, bool src_f32, int *threads, size_t *smem) {
+    *threads = kThreads;
+    *smem = 0;
+    if (mode == 1 && variant != 0) {
+        *threads = kThreads + 32;
+        *smem = src_f32 ? size_t(fp8_stages<true>()) * fp8_stage_bytes<true>()
+                        : size_t(fp8_stages<false>()) * fp8_stage_bytes<false>();
+    }
+}
+
+static cudaError_t prepare(const void *fn, size_t smem) {
+    if (smem == 0) return cudaSuccess;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+}
+
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream) {
+    const void *fn = kernel_for(mode, variant, src_f32);
+    int threads;
+    size_t smem;
+    launch_shape(mode, variant, src_f32, &threads, &smem);
     void *args[] = {const_cast<KParams *>(&P)};
-    return cudaLaunchKernel(kernel_for(mode, variant, src_f32), dim3(grid), dim3(kThreads), args, 0, stream);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
 }
 
 cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream) {
@@ -363,7 +507,13 @@ cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cud
 int sync_threads() { return kThreads; }
 
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kernel_for(mode, variant, src_f32), kThreads, 0);
+    const void *fn = kernel_for(mode, variant, src_f32);
+    int threads;
+    size_t smem;
+    launch_shape(mode, variant, src_f32, &threads, &smem);
+    cudaError_t e = prepare(fn, smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, threads, smem);
 }
 
 int num_cast_variants() { return kNumCastVariants; }

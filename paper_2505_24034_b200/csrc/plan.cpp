@@ -146,9 +146,18 @@ struct Builder {
         }
     }
 
-    // work lists per executing device, per destination device (for interleaving)
-    std::vector<std::vector<std::vector<Item>>> lists;   // [exec dev][dst dev]
-    std::vector<std::vector<std::vector<Seg>>> seglists;
+    // work lists per executing device, per destination device, per layer group
+    std::vector<std::vector<std::vector<std::vector<Item>>>> lists;   // [exec dev][dst dev][group]
+    std::vector<std::vector<Seg>> seglists;                           // [exec dev] (pull blocks)
+    int n_groups = 0;
+
+    // Layer groups (llrl_sync_group): [embed] | layer 0 | ... | layer L-1 | [final_norm + lm_head].
+    int group_of(int kind, int layer) const {
+        const int base = S->model.with_embed ? 1 : 0;
+        if (layer >= 0) return base + layer;
+        if (kind == LLRL_P_EMBED) return 0;
+        return n_groups - 1;
+    }
 
     void account(int exec, int sdev, int ddev, int64_t src_bytes, int64_t dst_bytes, bool pull) {
         const int G = P->n_devices;
@@ -168,13 +177,16 @@ struct Builder {
 
     llrl_status make_items() {
         const int G = P->n_devices;
-        lists.assign(G, std::vector<std::vector<Item>>(G));
-        seglists.assign(G, std::vector<std::vector<Seg>>(G));
+        n_groups = S->model.n_layers + (S->model.with_embed ? 2 : 0);
+        P->n_groups = n_groups;
+        lists.assign(G, std::vector<std::vector<std::vector<Item>>>(G, std::vector<std::vector<Item>>(n_groups)));
+        seglists.assign(G, {});
         // bf16 / f32 tiles
         for (const Tile &t : P->tiles) {
             if (t.quant) continue;
             const int sd = P->src_device[t.src_rank], dd = P->dst_device[t.dst_rank];
-            add_cast_items(t, lists[sd][dd]);
+            const SrcParam &sp = S->src_params[size_t(t.src_param)];
+            add_cast_items(t, lists[sd][dd][size_t(group_of(sp.kind, sp.layer))]);
             account(sd, sd, dd, t.rows * t.cols * es_src, t.rows * t.cols * es_dst, false);
         }
         // fp8 blocks: group quantised tiles by (dst rank, dst param)
@@ -185,6 +197,8 @@ struct Builder {
             const int g = kv.first.first;
             const Piece &pc = D->pieces[g][kv.first.second];
             const int dd = P->dst_device[g];
+            const DstParamDesc &dpd = D->dst_params[size_t(kv.first.second)];
+            const size_t grp = size_t(group_of(dpd.kind, dpd.layer));
             const int64_t nbr = (pc.rows + kFp8Block - 1) / kFp8Block, nbc = (pc.cols + kFp8Block - 1) / kFp8Block;
             for (int64_t bi = 0; bi < nbr; bi++)
                 for (int64_t bj = 0; bj < nbc; bj++) {
@@ -214,12 +228,12 @@ struct Builder {
                         const bool vec = it.cols % 16 == 0 && it.src_off % 8 == 0 && it.src_ld % 8 == 0 &&
                                          it.dst_off % 16 == 0 && it.dst_ld % 16 == 0;
                         it.flags = vec ? F_VEC : 0;
-                        lists[sd][dd].push_back(it);
+                        lists[sd][dd][grp].push_back(it);
                         account(sd, sd, dd, B.area() * es_src, B.area() + 4, false);
                     } else {
                         it.kind = K_FP8_MULTI;
                         P->stats.n_fp8_pull_blocks++;
-                        auto &sl = seglists[dd][dd];
+                        auto &sl = seglists[dd];
                         it.src_off = int64_t(sl.size());
                         it.src_rank = uint16_t(segs.size());   // segment count
                         for (auto &s : segs) {
@@ -237,51 +251,98 @@ struct Builder {
                             account(dd, P->src_device[t.src_rank], dd, I.area() * es_src, 0, true);
                         }
                         account(dd, dd, dd, 0, B.area() + 4, false);
-                        P->stats.src_bytes += 0;
-                        lists[dd][dd].push_back(it);
+                        lists[dd][dd][grp].push_back(it);
                     }
                 }
         }
-        // interleave per executing device by fractional progress through each destination list
+        // Per executing device and layer group: interleave the destination lists by
+        // fractional progress (every NVLink peer and the local copy advance
+        // together), then lay the items out as [cast items | fp8 items], each
+        // class group-major, with per-group offsets for llrl_sync_group.
+        auto item_bytes = [](const Item &it) { return double(it.rows) * double(it.cols); };
         for (int e = 0; e < G; e++) {
             DeviceWork &W = P->dev[e];
-            // segments: only pull items (dst == exec) use them
-            W.segs = std::move(seglists[e][e]);
-            struct Cursor { int dst; size_t pos; double total, done; };
-            std::vector<Cursor> cur;
-            auto item_bytes = [](const Item &it) { return double(it.rows) * double(it.cols); };
-            for (int d = 0; d < G; d++) {
-                if (lists[e][d].empty()) continue;
-                double tot = 0;
-                for (auto &it : lists[e][d]) tot += item_bytes(it);
-                // rotate the start by the executing device so senders spread over receivers
-                cur.push_back({d, 0, tot, 0});
-                if (d != e) W.signal_devices.push_back(d);
-            }
-            std::rotate(cur.begin(), cur.begin() + (cur.empty() ? 0 : size_t(e) % cur.size()), cur.end());
-            size_t n_total = 0;
-            for (auto &c : cur) n_total += lists[e][c.dst].size();
-            W.items.reserve(n_total);
-            while (W.items.size() < n_total) {
-                Cursor *best = nullptr;
-                double best_frac = 2.0;
-                for (auto &c : cur) {
-                    if (c.pos >= lists[e][c.dst].size()) continue;
-                    const double f = c.done / c.total;
-                    if (f < best_frac) { best_frac = f; best = &c; }
+            W.segs = std::move(seglists[e]);
+            std::vector<std::vector<Item>> cast_g(static_cast<size_t>(n_groups)), fp8_g(static_cast<size_t>(n_groups));
+            W.group_signal.assign(size_t(n_groups), {});
+            std::vector<char> sends(size_t(G), 0);
+            for (int grp = 0; grp < n_groups; grp++) {
+                struct Cursor { int dst; size_t pos; double total, done; };
+                std::vector<Cursor> cur;
+                for (int d = 0; d < G; d++) {
+                    const auto &L = lists[e][d][size_t(grp)];
+                    if (L.empty()) continue;
+                    double tot = 0;
+                    for (auto &it : L) tot += item_bytes(it);
+                    cur.push_back({d, 0, tot, 0});
+                    if (d != e) { W.group_signal[size_t(grp)].push_back(d); sends[size_t(d)] = 1; }
                 }
-                const Item &it = lists[e][best->dst][best->pos++];
-                best->done += item_bytes(it);
-                W.items.push_back(it);
+                // rotate the start by the executing device so senders spread over receivers
+                if (!cur.empty()) std::rotate(cur.begin(), cur.begin() + size_t(e) % cur.size(), cur.end());
+                size_t n_total = 0, n_done = 0;
+                for (auto &c : cur) n_total += lists[e][c.dst][size_t(grp)].size();
+                while (n_done < n_total) {
+                    Cursor *best = nullptr;
+                    double best_frac = 2.0;
+                    for (auto &c : cur) {
+                        if (c.pos >= lists[e][c.dst][size_t(grp)].size()) continue;
+                        const double f = c.done / c.total;
+                        if (f < best_frac) { best_frac = f; best = &c; }
+                    }
+                    const Item &it = lists[e][best->dst][size_t(grp)][best->pos++];
+                    best->done += item_bytes(it);
+                    (it.kind == K_CAST ? cast_g : fp8_g)[size_t(grp)].push_back(it);
+                    n_done++;
+                }
             }
-            // [cast items | fp8 items]: one launch per class (different register budgets)
-            auto mid = std::stable_partition(W.items.begin(), W.items.end(),
-                                             [](const Item &it) { return it.kind == K_CAST; });
-            W.n_cast = int64_t(mid - W.items.begin());
+            W.cast_off.assign(size_t(n_groups) + 1, 0);
+            W.fp8_off.assign(size_t(n_groups) + 1, 0);
+            for (int grp = 0; grp < n_groups; grp++) {
+                W.cast_off[size_t(grp)] = int64_t(W.items.size());
+                W.items.insert(W.items.end(), cast_g[size_t(grp)].begin(), cast_g[size_t(grp)].end());
+            }
+            W.n_cast = int64_t(W.items.size());
+            W.cast_off[size_t(n_groups)] = W.n_cast;
+            for (int grp = 0; grp < n_groups; grp++) {
+                W.fp8_off[size_t(grp)] = int64_t(W.items.size());
+                W.items.insert(W.items.end(), fp8_g[size_t(grp)].begin(), fp8_g[size_t(grp)].end());
+            }
+            W.fp8_off[size_t(n_groups)] = int64_t(W.items.size());
+            for (int d = 0; d < G; d++)
+                if (sends[size_t(d)]) W.signal_devices.push_back(d);
             P->stats.n_items += int64_t(W.items.size());
         }
-        for (int e = 0; e < G; e++)
-            for (int d : P->dev[e].signal_devices) P->dev[d].n_senders_in++;
+        for (int e = 0; e < G; e++) {
+            P->dev[size_t(e)].group_senders_in.assign(size_t(n_groups), 0);
+        }
+        for (int e = 0; e < G; e++) {
+            for (int d : P->dev[size_t(e)].signal_devices) P->dev[size_t(d)].n_senders_in++;
+            for (int grp = 0; grp < n_groups; grp++)
+                for (int d : P->dev[size_t(e)].group_signal[size_t(grp)]) P->dev[size_t(d)].group_senders_in[size_t(grp)]++;
+        }
+        // per-group byte ranges of every rank buffer (host <-> device streaming)
+        P->src_group_range.assign(size_t(S->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));
+        P->dst_group_range.assign(size_t(D->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));
+        auto widen = [](std::pair<int64_t, int64_t> &r, int64_t lo, int64_t hi) {
+            if (hi <= lo) return;
+            if (r.first < 0) r = {lo, hi};
+            else r = {std::min(r.first, lo), std::max(r.second, hi)};
+        };
+        for (int r = 0; r < S->n_ranks; r++)
+            for (const Piece &pc : S->pieces[size_t(r)]) {
+                const SrcParam &sp = S->src_params[size_t(pc.param)];
+                widen(P->src_group_range[size_t(r)][size_t(group_of(sp.kind, sp.layer))], pc.byte_off,
+                      pc.byte_off + pc.rows * pc.cols * es_src);
+            }
+        for (int g = 0; g < D->n_ranks; g++)
+            for (const Piece &pc : D->pieces[size_t(g)]) {
+                const DstParamDesc &dpd = D->dst_params[size_t(pc.param)];
+                auto &rg = P->dst_group_range[size_t(g)][size_t(group_of(dpd.kind, dpd.layer))];
+                widen(rg, pc.byte_off, pc.byte_off + pc.rows * pc.cols * dtype_bytes(pc.dtype));
+                if (pc.quantised)
+                    widen(rg, pc.scale_off, pc.scale_off + ((pc.rows + kFp8Block - 1) / kFp8Block) *
+                                                               ((pc.cols + kFp8Block - 1) / kFp8Block) * 4);
+            }
         return LLRL_OK;
     }
 };

@@ -59,15 +59,17 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     W.variant = kDefaultCastVariant;
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
+    W.fp8_variant = 1;                                                       // TMA pipeline
+    if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = atoi(v) ? 1 : 0;
     for (int mode = 0; mode < 2; mode++) {
         int per_sm = 0;
-        CK(sync_occupancy(mode, W.variant, p->src_dtype == LLRL_F32, &per_sm));
+        CK(sync_occupancy(mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, &per_sm));
         if (per_sm < 1) per_sm = 1;
         const int64_t n = mode == 0 ? n_cast : n_fp8;
         const int g = int(std::min<int64_t>(int64_t(sms) * per_sm, std::max<int64_t>(1, n)));
         (mode == 0 ? W.grid_cast : W.grid_fp8) = g;
     }
-    W.epoch = 0;
+    W.done_total = 0;
     W.uploaded_device = device;
     return LLRL_OK;
 }
@@ -88,13 +90,15 @@ void touched_ranks(const DeviceWork &W, std::vector<char> &src, std::vector<char
 
 extern "C" {
 
-llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs, void *const *dst_ptrs,
-                      void *stream) {
+// Common prologue of llrl_sync / llrl_sync_group / llrl_sync_host: validate,
+// fill the pointer tables, upload on first use.
+static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs,
+                            void *const *dst_ptrs, KParams *kp) {
     if (!p || !src_ptrs || !dst_ptrs || device < 0 || device >= p->n_devices) {
         set_error("llrl_sync: invalid argument (device %d of %d)", device, p ? p->n_devices : 0);
         return LLRL_E_INVALID;
     }
-    DeviceWork &W = p->dev[device];
+    DeviceWork &W = p->dev[size_t(device)];
     const bool cross = !W.signal_devices.empty() || W.n_senders_in > 0;
     if (cross) {
         if (!comm || comm->device != device) {
@@ -109,48 +113,88 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
     }
     std::vector<char> su(size_t(p->n_src), 0), du(size_t(p->n_dst), 0);
     touched_ranks(W, su, du);
-    KParams kp;
-    std::memset(&kp, 0, sizeof kp);
+    std::memset(kp, 0, sizeof *kp);
     for (int r = 0; r < p->n_src; r++) {
-        if (su[r] && !src_ptrs[r]) { set_error("llrl_sync: src_ptrs[%d] is NULL", r); return LLRL_E_NOPEER; }
-        kp.src[r] = src_ptrs[r];
+        if (su[size_t(r)] && !src_ptrs[r]) { set_error("llrl_sync: src_ptrs[%d] is NULL", r); return LLRL_E_NOPEER; }
+        kp->src[r] = src_ptrs[r];
     }
     for (int g = 0; g < p->n_dst; g++) {
-        if (du[g] && !dst_ptrs[g]) { set_error("llrl_sync: dst_ptrs[%d] is NULL", g); return LLRL_E_NOPEER; }
-        kp.dst[g] = dst_ptrs[g];
+        if (du[size_t(g)] && !dst_ptrs[g]) { set_error("llrl_sync: dst_ptrs[%d] is NULL", g); return LLRL_E_NOPEER; }
+        kp->dst[g] = dst_ptrs[g];
     }
-    DeviceGuard guard(device);
     llrl_status st = ensure_uploaded(p, device);
     if (st != LLRL_OK) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!W.items.empty()) {
-        W.epoch++;
-        kp.items = W.d_items;
-        kp.segs = W.d_segs;
-        const int64_t n = int64_t(W.items.size());
-        const bool has_cast = W.n_cast > 0, has_fp8 = n > W.n_cast;
-        for (int mode = 0; mode < 2; mode++) {
-            if (mode == 0 ? !has_cast : !has_fp8) continue;
-            const bool last = mode == 1 || !has_fp8;
-            const int grid = mode == 0 ? W.grid_cast : W.grid_fp8;
-            kp.item_begin = mode == 0 ? 0 : int(W.n_cast);
-            kp.item_end = mode == 0 ? int(W.n_cast) : int(n);
-            kp.done = nullptr;
-            kp.n_signal = 0;
-            if (last && !W.signal_devices.empty()) {
-                kp.done = W.d_done;
-                kp.done_target = W.epoch * uint64_t(grid);
-                kp.n_signal = int(W.signal_devices.size());
-                for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[W.signal_devices[i]];
-            }
-            CK(launch_sync(kp, mode, W.variant, p->src_dtype == LLRL_F32, grid, s));
+    kp->items = W.d_items;
+    kp->segs = W.d_segs;
+    return LLRL_OK;
+}
+
+// Enqueue cast items [c0, c1) and fp8 items [f0, f1); the last launch signals
+// every device in `sig` (its last CTA, after all CTAs' stores are fenced).
+static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, KParams &kp, int64_t c0, int64_t c1,
+                                 int64_t f0, int64_t f1, const std::vector<int> &sig, cudaStream_t s) {
+    const bool has_fp8 = f1 > f0;
+    for (int mode = 0; mode < 2; mode++) {
+        const int64_t b = mode == 0 ? c0 : f0, e = mode == 0 ? c1 : f1;
+        if (e <= b) continue;
+        const bool last = mode == 1 || !has_fp8;
+        const int grid = int(std::min<int64_t>(mode == 0 ? W.grid_cast : W.grid_fp8, e - b));
+        kp.item_begin = int(b);
+        kp.item_end = int(e);
+        kp.done = nullptr;
+        kp.n_signal = 0;
+        if (last && !sig.empty()) {
+            W.done_total += uint64_t(grid);
+            kp.done = W.d_done;
+            kp.done_target = W.done_total;
+            kp.n_signal = int(sig.size());
+            for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]];
         }
-    }
-    if (W.n_senders_in > 0) {
-        comm->expected += uint64_t(W.n_senders_in);
-        CK(launch_wait(comm->flags, comm->expected, s));
+        CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
     }
     return LLRL_OK;
+}
+
+static llrl_status wait_arrivals(llrl_comm *comm, int n, cudaStream_t s) {
+    if (n <= 0) return LLRL_OK;
+    comm->expected += uint64_t(n);
+    CK(launch_wait(comm->flags, comm->expected, s));
+    return LLRL_OK;
+}
+
+llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs, void *const *dst_ptrs,
+                      void *stream) {
+    DeviceGuard guard(device >= 0 ? device : 0);
+    KParams kp;
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
+    if (st != LLRL_OK) return st;
+    DeviceWork &W = p->dev[size_t(device)];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    st = launch_ranges(p, W, comm, kp, 0, W.n_cast, W.n_cast, int64_t(W.items.size()), W.signal_devices, s);
+    if (st != LLRL_OK) return st;
+    return wait_arrivals(comm, W.n_senders_in, s);
+}
+
+llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n) {
+    if (!p || !n) { set_error("NULL argument"); return LLRL_E_INVALID; }
+    *n = p->n_groups;
+    return LLRL_OK;
+}
+
+llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group, void *const *src_ptrs,
+                            void *const *dst_ptrs, void *stream) {
+    if (!p || group < 0 || group >= p->n_groups) { set_error("llrl_sync_group: invalid group"); return LLRL_E_INVALID; }
+    DeviceGuard guard(device >= 0 ? device : 0);
+    KParams kp;
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
+    if (st != LLRL_OK) return st;
+    DeviceWork &W = p->dev[size_t(device)];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t g = size_t(group);
+    st = launch_ranges(p, W, comm, kp, W.cast_off[g], W.cast_off[g + 1], W.fp8_off[g], W.fp8_off[g + 1],
+                       W.group_signal[g], s);
+    if (st != LLRL_OK) return st;
+    return wait_arrivals(comm, W.group_senders_in[g], s);
 }
 
 llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n) {
@@ -173,22 +217,67 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
     return llrl_sync_num_launches(p, device, &out->n_launches);
 }
 
+// Host-buffer entry: per layer group, H2D of the group's trainer bytes (copy
+// stream) -> the group's kernels (+ completion) on `stream` -> D2H of the
+// group's generator bytes (second copy stream), so PCIe traffic in both
+// directions overlaps the kernels of neighbouring groups.
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void *const *host_src,
                            void *const *host_dst, void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
-    if (!p || !host_src || !host_dst || !src_ptrs || !dst_ptrs || device < 0 || device >= p->n_devices) {
-        set_error("llrl_sync_host: invalid argument");
-        return LLRL_E_INVALID;
-    }
-    DeviceGuard guard(device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    for (int r = 0; r < p->n_src; r++)
-        if (p->src_device[r] == device && host_src[r])
-            CK(cudaMemcpyAsync(src_ptrs[r], host_src[r], size_t(p->src_rank_bytes[r]), cudaMemcpyHostToDevice, s));
-    llrl_status st = llrl_sync(p, comm, device, src_ptrs, dst_ptrs, stream);
+    if (!host_src || !host_dst) { set_error("llrl_sync_host: invalid argument"); return LLRL_E_INVALID; }
+    DeviceGuard guard(device >= 0 ? device : 0);
+    KParams kp;
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
     if (st != LLRL_OK) return st;
-    for (int g = 0; g < p->n_dst; g++)
-        if (p->dst_device[g] == device && host_dst[g])
-            CK(cudaMemcpyAsync(host_dst[g], dst_ptrs[g], size_t(p->dst_rank_bytes[g]), cudaMemcpyDeviceToHost, s));
+    DeviceWork &W = p->dev[size_t(device)];
+    const int G = p->n_groups;
+    if (!W.h2d_stream) {
+        cudaStream_t a, b;
+        CK(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        W.h2d_stream = a;
+        W.d2h_stream = b;
+        W.events.resize(size_t(2 * G + 2));
+        for (auto &e : W.events) {
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            e = ev;
+        }
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaStream_t h2d = static_cast<cudaStream_t>(W.h2d_stream), d2h = static_cast<cudaStream_t>(W.d2h_stream);
+    auto ev = [&](size_t i) { return static_cast<cudaEvent_t>(W.events[i]); };
+    // copies must not overtake work already queued on `stream` (previous sync)
+    CK(cudaEventRecord(ev(size_t(2 * G)), s));
+    CK(cudaStreamWaitEvent(h2d, ev(size_t(2 * G)), 0));
+    CK(cudaStreamWaitEvent(d2h, ev(size_t(2 * G)), 0));
+    for (int g = 0; g < G; g++) {
+        for (int r = 0; r < p->n_src; r++) {
+            const auto &rg = p->src_group_range[size_t(r)][size_t(g)];
+            if (p->src_device[size_t(r)] != device || !host_src[r] || rg.first < 0) continue;
+            CK(cudaMemcpyAsync(static_cast<char *>(src_ptrs[r]) + rg.first,
+                               static_cast<const char *>(host_src[r]) + rg.first, size_t(rg.second - rg.first),
+                               cudaMemcpyHostToDevice, h2d));
+        }
+        CK(cudaEventRecord(ev(size_t(2 * g)), h2d));
+        CK(cudaStreamWaitEvent(s, ev(size_t(2 * g)), 0));
+        const size_t gg = size_t(g);
+        st = launch_ranges(p, W, comm, kp, W.cast_off[gg], W.cast_off[gg + 1], W.fp8_off[gg], W.fp8_off[gg + 1],
+                           W.group_signal[gg], s);
+        if (st != LLRL_OK) return st;
+        st = wait_arrivals(comm, W.group_senders_in[gg], s);
+        if (st != LLRL_OK) return st;
+        CK(cudaEventRecord(ev(size_t(2 * g + 1)), s));
+        CK(cudaStreamWaitEvent(d2h, ev(size_t(2 * g + 1)), 0));
+        for (int q = 0; q < p->n_dst; q++) {
+            const auto &rg = p->dst_group_range[size_t(q)][gg];
+            if (p->dst_device[size_t(q)] != device || !host_dst[q] || rg.first < 0) continue;
+            CK(cudaMemcpyAsync(static_cast<char *>(host_dst[q]) + rg.first,
+                               static_cast<const char *>(dst_ptrs[q]) + rg.first, size_t(rg.second - rg.first),
+                               cudaMemcpyDeviceToHost, d2h));
+        }
+    }
+    CK(cudaEventRecord(ev(size_t(2 * G + 1)), d2h));
+    CK(cudaStreamWaitEvent(s, ev(size_t(2 * G + 1)), 0));
     return LLRL_OK;
 }
 
@@ -201,6 +290,9 @@ void llrl_plan_destroy(llrl_plan *p) {
         cudaFree(W.d_items);
         cudaFree(W.d_segs);
         cudaFree(W.d_done);
+        for (void *e : W.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+        if (W.h2d_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.h2d_stream));
+        if (W.d2h_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.d2h_stream));
     }
     delete p;
 }

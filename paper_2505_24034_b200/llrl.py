@@ -32,7 +32,7 @@ EXPORTS = [
     "llrl_plan_num_runs", "llrl_plan_get_runs", "llrl_plan_stats_get", "llrl_plan_traffic",
     "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
     "llrl_comm_set_peer", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
-    "llrl_sync", "llrl_sync_host", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_last_error",
+    "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_last_error",
     "llrl_version",
 ]
 
@@ -106,6 +106,8 @@ _sig("llrl_ipc_handle", [_vp, ctypes.c_char_p, _P(_i64)])
 _sig("llrl_ipc_open", [ctypes.c_char_p, _i64, _P(_vp)])
 _sig("llrl_ipc_close", [_vp, _i64])
 _sig("llrl_sync", [_vp, _vp, _int, _P(_vp), _P(_vp), _vp])
+_sig("llrl_plan_num_groups", [_vp, _P(_int)])
+_sig("llrl_sync_group", [_vp, _vp, _int, _int, _P(_vp), _P(_vp), _vp])
 _sig("llrl_sync_host", [_vp, _vp, _int, _P(_vp), _P(_vp), _P(_vp), _P(_vp), _vp])
 _sig("llrl_sync_num_launches", [_vp, _int, _P(_int)])
 _sig("llrl_fill_synthetic", [_vp, _int, _vp, ctypes.c_uint64, _vp])
@@ -234,6 +236,16 @@ class Plan:
         """llrl_sync: enqueue this device's share of the sync on `stream` (int handle)."""
         _check(_lib.llrl_sync(self._h, comm.handle if comm else None, device, _ptrs(src_ptrs), _ptrs(dst_ptrs),
                               _vp(stream)))
+
+    def num_groups(self):
+        n = _int()
+        _check(_lib.llrl_plan_num_groups(self._h, ctypes.byref(n)))
+        return n.value
+
+    def sync_group(self, comm, device, group, src_ptrs, dst_ptrs, stream):
+        """llrl_sync_group: this device's share of one layer group."""
+        _check(_lib.llrl_sync_group(self._h, comm.handle if comm else None, device, group, _ptrs(src_ptrs),
+                                    _ptrs(dst_ptrs), _vp(stream)))
 
     def sync_host(self, comm, device, host_src, host_dst, src_ptrs, dst_ptrs, stream):
         _check(_lib.llrl_sync_host(self._h, comm.handle if comm else None, device, _ptrs(host_src),

@@ -47,6 +47,31 @@ def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, se
             if not np.array_equal(got, want[g]):
                 bad = np.nonzero(got != want[g])[0]
                 raise AssertionError(f"{cfg} rep {rep}: dst rank {g} differs at {bad.size} bytes, first {bad[:6]}")
+    # layer-group streaming and the host-buffer entry across GPUs
+    src = harness.host_src(ol, seed + 50)
+    for r, t in job.src.items():
+        t.copy_(torch.from_numpy(src[r]))
+    for t in job.dst.values():
+        t.fill_(0x5A)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for grp in range(job.plan.num_groups()):
+        job.plan.sync_group(job.comm, job.device, grp, job.src_ptrs, job.dst_ptrs, job.stream.cuda_stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    want = harness.oracle_dst(ol, src, 0x5A)
+    for g, t in job.dst.items():
+        assert np.array_equal(t.cpu().numpy(), want[g]), f"{cfg} sync_group: dst rank {g}"
+    src = harness.host_src(ol, seed + 60)
+    hs = {r: torch.from_numpy(src[r]).pin_memory() for r in job.src}
+    hd = {g: torch.full((job.D.rank_bytes(g),), 0x5A, dtype=torch.uint8).pin_memory() for g in job.dst}
+    dist.barrier()
+    job.sync_host(hs, hd)
+    torch.cuda.synchronize()
+    dist.barrier()
+    want = harness.oracle_dst(ol, src, 0x5A)
+    for g in job.dst:
+        assert np.array_equal(hd[g].numpy(), want[g]), f"{cfg} sync_host: dst rank {g}"
     job.close()
 
 

@@ -216,3 +216,57 @@ def test_toy_parity_cast_variants(rt, variant, monkeypatch):
         job = _toy_job(rt, "toy", f, tt, tg, sdt, ddt)
         _run_and_compare(rt, job, seed=variant)
         job.close()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_toy_parity_fp8_variants(rt, variant, monkeypatch):
+    """Both fp8 kernels (register / TMA-pipelined, LLRL_FP8_VARIANT) are bit-exact,
+    including multi-source (pull) blocks and partial edge blocks."""
+    monkeypatch.setenv("LLRL_FP8_VARIANT", str(variant))
+    for sdt, f, tt, tg in (("bf16", 1, 8, 8), ("f32", 3, 1, 4), ("bf16", 2, 2, 8), ("f32", 2, 1, 2)):
+        job = _toy_job(rt, "toy", f, tt, tg, sdt, "fp8")
+        _run_and_compare(rt, job, seed=40 + variant)
+        job.close()
+
+
+@pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8), ("f32", "fp8", 3, 1, 4)])
+def test_toy_parity_sync_group(rt, sdt, ddt, f, tt, tg):
+    """llrl_sync_group over every layer group (in reverse order) == the whole sync."""
+    job = _toy_job(rt, "toy", f, tt, tg, sdt, ddt)
+    ol = oracle.Layout(job.model, f, tt, tg, sdt, ddt)
+    src = harness.host_src(ol, 77)
+    for r, t in job.src.items():
+        t.copy_(torch.from_numpy(src[r]))
+    for t in job.dst.values():
+        t.fill_(0x33)
+    n = job.plan.num_groups()
+    assert n == job.model.n_layers + 2
+    for grp in reversed(range(n)):
+        job.plan.sync_group(job.comm, job.device, grp, job.src_ptrs, job.dst_ptrs, job.stream.cuda_stream)
+    torch.cuda.synchronize()
+    want = harness.oracle_dst(ol, src, 0x33)
+    for g, t in job.dst.items():
+        assert np.array_equal(t.cpu().numpy(), want[g]), g
+    job.close()
+
+
+@pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8)])
+def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
+    """llrl_sync_host: pinned host trainer shards in, host generator shards out,
+    pipelined per layer group; twice, to exercise stream/event reuse."""
+    job = _toy_job(rt, "toy", f, tt, tg, sdt, ddt)
+    ol = oracle.Layout(job.model, f, tt, tg, sdt, ddt)
+    for rep in range(2):
+        src = harness.host_src(ol, 90 + rep)
+        hs = {r: torch.from_numpy(src[r]).pin_memory() for r in job.src}
+        hd = {g: torch.full((job.D.rank_bytes(g),), 0x44, dtype=torch.uint8).pin_memory() for g in job.dst}
+        for t in job.src.values():
+            t.fill_(0)                # the device copy must come from the host buffers
+        for t in job.dst.values():
+            t.fill_(0x44)             # padding inside a group's range travels back too
+        job.sync_host(hs, hd)
+        torch.cuda.synchronize()
+        want = harness.oracle_dst(ol, src, 0x44)
+        for g in job.dst:
+            assert np.array_equal(hd[g].numpy(), want[g]), (rep, g)
+    job.close()
