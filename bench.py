@@ -217,6 +217,8 @@ def run_llrl(args):
     world, rank, local = _dist_setup(args)
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
     spec = runner.spec_for(args.config, args.gpus)
+    if args.layers is not None:           # profiling only (ncu replay of a smaller model)
+        spec = runner.JobSpec(spec.cfg, spec.n_gpus, n_layers=args.layers)
     job = runner.SyncJob(spec, device=local, seed=0)
     cfg = job.cfg
     stream = job.stream
@@ -363,6 +365,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=None, help="override decoder layers (profiling only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -126,6 +126,17 @@ struct alignas(16) Seg {
 };
 static_assert(sizeof(Seg) == 32, "Seg layout");
 
+// fp8 block source as a 2-D TMA tile: tensor map `map` (one per source piece)
+// and the block's top-left (x = column, y = row) inside that piece.  map < 0:
+// no tensor map (stride not 16-byte aligned); the kernel stages row by row.
+struct TmaRef {
+    int32_t map, x, y, pad;
+};
+struct TmaPiece {            // a trainer piece that fp8 blocks read through a tensor map
+    int src_rank;
+    int64_t byte_off, rows, cols;
+};
+
 // Host-side tile: one rectangle intersection (param part, src rank, dst rank).
 struct Tile {
     int src_param;
@@ -141,6 +152,8 @@ struct Tile {
 struct DeviceWork {
     std::vector<Item> items;
     std::vector<Seg> segs;
+    std::vector<TmaRef> tma_refs;      // one per fp8 item (index i - n_cast)
+    std::vector<TmaPiece> tma_pieces;
     std::vector<int> signal_devices;   // devices this device writes into (excl. itself)
     int n_senders_in = 0;              // other devices writing into this device
     // layer groups: items [cast_off[g], cast_off[g+1]) and [fp8_off[g], fp8_off[g+1])
@@ -152,6 +165,10 @@ struct DeviceWork {
     int uploaded_device = -1;
     Item *d_items = nullptr;
     Seg *d_segs = nullptr;
+    TmaRef *d_tma_refs = nullptr;
+    void *d_tmaps = nullptr;                // CUtensorMap[tma_pieces.size()] (64-byte aligned)
+    std::vector<unsigned char> h_tmaps;     // host copy (kept alive for the async upload)
+    std::vector<const void *> tmap_src;     // src base pointers the maps were encoded for
     unsigned long long *d_done = nullptr;   // last-CTA counter (cumulative)
     uint64_t done_total = 0;                // CTAs of all signalling launches so far
     void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)

@@ -372,13 +372,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
                  : "memory");
 }
 
+// 2-D tensor TMA: one 128x128 box of the piece's tensor map at (x, y); rows /
+// columns outside the piece are zero-filled (never used: workers mask).
+__device__ __forceinline__ void tma_box_g2s(void *dst_smem, const void *tmap, int x, int y, uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(smem_u32(dst_smem)), "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 template <bool SRC_F32>
-__host__ __device__ constexpr int fp8_stages() { return SRC_F32 ? 3 : 5; }
+__host__ __device__ constexpr int fp8_stages() { return SRC_F32 ? 3 : 3; }
 template <bool SRC_F32>
 __host__ __device__ constexpr int fp8_stage_bytes() { return 128 * 128 * (SRC_F32 ? 4 : 2); }
 
 template <bool SRC_F32>
-__global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_fp8_tma(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_constant__ KParams P) {
     constexpr int S = fp8_stages<SRC_F32>();
     constexpr int kStage = fp8_stage_bytes<SRC_F32>();
     constexpr int es = SRC_F32 ? 4 : 2;
@@ -403,13 +412,22 @@ __global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_fp8_tma(const __grid_
             mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
             const Item it = P.items[i];
             const bool tma = it.kind == K_FP8 && (it.flags & F_VEC);
+            const TmaRef ref = tma ? P.tma_refs[i - P.fp8_base] : TmaRef{-1, 0, 0, 0};
             if (lane == 0) {
                 slot[st] = it;
-                if (tma) mbar_arrive_tx(&full_bar[st], uint32_t(it.rows * it.cols * es));
-                else mbar_arrive(&full_bar[st]);
+                if (tma && ref.map >= 0) {
+                    // the whole 128x128 box lands (zero-filled outside the piece)
+                    mbar_arrive_tx(&full_bar[st], uint32_t(kStage));
+                    tma_box_g2s(stages + st * kStage, static_cast<const unsigned char *>(P.tmaps) + 128 * ref.map,
+                                ref.x, ref.y, &full_bar[st]);
+                } else if (tma) {
+                    mbar_arrive_tx(&full_bar[st], uint32_t(it.rows * it.cols * es));
+                } else {
+                    mbar_arrive(&full_bar[st]);
+                }
             }
             __syncwarp();
-            if (tma) {
+            if (tma && ref.map < 0) {
                 const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
                 for (int r = lane; r < it.rows; r += 32)
                     bulk_g2s(stages + st * kStage + r * 128 * es, src + int64_t(r) * it.src_ld * es,
@@ -429,6 +447,176 @@ __global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_fp8_tma(const __grid_
                 fp8_item_generic<SRC_F32>(it, P, s_red[k & 1]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+    }
+    complete(P);
+}
+
+// ---- K1b: TMA-staged relayout + cast ---------------------------------------------
+// Warp-specialised like K2: warp 0 (producer) stages each item's rows into a
+// kCastStages-deep ring of 32 KiB shared-memory stages with cp.async.bulk
+// (mbarrier tx-count completion); warps 1..4 (workers) convert fp32 -> bf16
+// in shared memory when a cast is needed, and one worker thread writes each
+// stage back with cp.async.bulk shared -> global (local HBM or a peer GPU's
+// HBM over NVLink), releasing a stage once its bulk store has read it.  Data
+// never passes through registers on identity copies (bf16 -> bf16).
+
+constexpr int kCastStageBytes = 32 * 1024;
+constexpr int kCastStages = 4;
+constexpr int kCastWorkers = 128;
+
+// Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
+// item, at most kCastStageBytes of source.  Same enumeration on both roles.
+struct Chunk {
+    int r0, nr, c0, nc;
+};
+__device__ __forceinline__ int cast_chunks(const Item &it, int es, int *rows_per, int *segs_per_row) {
+    const int row_bytes = it.cols * es;
+    if (row_bytes <= kCastStageBytes) {
+        *rows_per = kCastStageBytes / row_bytes;
+        *segs_per_row = 1;
+        return (it.rows + *rows_per - 1) / *rows_per;
+    }
+    *rows_per = 1;
+    *segs_per_row = (row_bytes + kCastStageBytes - 1) / kCastStageBytes;
+    return it.rows * *segs_per_row;
+}
+__device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per, int segs_per_row, int k) {
+    Chunk c;
+    if (segs_per_row == 1) {
+        c.r0 = k * rows_per;
+        c.nr = min(rows_per, it.rows - c.r0);
+        c.c0 = 0;
+        c.nc = it.cols;
+    } else {
+        const int seg_elems = kCastStageBytes / es;
+        c.r0 = k / segs_per_row;
+        c.nr = 1;
+        c.c0 = (k % segs_per_row) * seg_elems;
+        c.nc = min(seg_elems, it.cols - c.c0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(smem_u32(src_smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cast_workers_sync() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+
+template <bool SRC_F32>
+__global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {
+    constexpr int es = SRC_F32 ? 4 : 2;
+    extern __shared__ __align__(128) unsigned char stages[];   // kCastStages x (in 32 KiB [+ out 16 KiB])
+    constexpr int kOut = SRC_F32 ? kCastStageBytes / 2 : 0;
+    constexpr int kStride = kCastStageBytes + kOut;
+    __shared__ __align__(8) uint64_t full_bar[kCastStages], empty_bar[kCastStages];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kCastStages; s++) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // producer: stage rows of every vector item; scalar items pass a token
+        int n = 0;
+        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+            const Item it = P.items[i];
+            int rows_per, segs;
+            const int nch = (it.flags & F_VEC) ? cast_chunks(it, es, &rows_per, &segs) : 1;
+            const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+                if (!(it.flags & F_VEC)) {
+                    if (lane == 0) mbar_arrive(&full_bar[st]);
+                    continue;
+                }
+                const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
+                __syncwarp();
+                unsigned char *dst = stages + st * kStride;
+                for (int r = lane; r < c.nr; r += 32)
+                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                             uint32_t(c.nc * es), &full_bar[st]);
+            }
+        }
+    } else {
+        // workers: (cast in smem), one thread stores each stage back with bulk copies
+        const int wt = threadIdx.x - 32;
+        const bool leader = wt == 0;
+        int n = 0, pend_stage = -1;
+        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+            const Item it = P.items[i];
+            const bool dst_f32 = it.flags & F_DST_F32;
+            char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
+            if (!(it.flags & F_VEC)) {
+                const int st = n % kCastStages;
+                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+                const char *src = static_cast<const char *>(P.src[it.src_rank]);
+                const int ne = it.rows * it.cols;
+                for (int e = wt; e < ne; e += kCastWorkers) {
+                    const int r = e / it.cols, c = e - r * it.cols;
+                    const int64_t so = it.src_off + int64_t(r) * it.src_ld + c;
+                    const int64_t dof = it.dst_off + int64_t(r) * it.dst_ld + c;
+                    if (SRC_F32) {
+                        const uint32_t x = *reinterpret_cast<const uint32_t *>(src + so * 4);
+                        if (dst_f32) *reinterpret_cast<uint32_t *>(dbase + dof * 4) = x;
+                        else *reinterpret_cast<uint16_t *>(dbase + dof * 2) = bf16_rn(__uint_as_float(x));
+                    } else {
+                        *reinterpret_cast<uint16_t *>(dbase + dof * 2) = *reinterpret_cast<const uint16_t *>(src + so * 2);
+                    }
+                }
+                cast_workers_sync();
+                if (leader) mbar_arrive(&empty_bar[st]);
+                n++;
+                continue;
+            }
+            int rows_per, segs;
+            const int nch = cast_chunks(it, es, &rows_per, &segs);
+            const bool cast = SRC_F32 && !dst_f32;
+            const int des = cast ? 2 : es;
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+                const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                unsigned char *in = stages + st * kStride;
+                unsigned char *out = in;
+                if (cast) {
+                    out = in + kCastStageBytes;
+                    const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
+                    for (int u = wt; u < nunits; u += kCastWorkers) {
+                        const uint4 a = reinterpret_cast<const uint4 *>(in)[u];
+                        reinterpret_cast<uint2 *>(out)[u] =
+                            make_uint2(bf16x2_rn(__uint_as_float(a.x), __uint_as_float(a.y)),
+                                       bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    cast_workers_sync();
+                }
+                if (leader) {
+                    for (int r = 0; r < c.nr; r++)
+                        bulk_s2g(dbase + (it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0) * des,
+                                 out + r * c.nc * des, uint32_t(c.nc * des));
+                    bulk_commit();
+                    // release the previous stage once its store has read shared memory
+                    bulk_wait_read<1>();
+                    if (pend_stage >= 0) mbar_arrive(&empty_bar[pend_stage]);
+                    pend_stage = st;
+                }
+            }
+        }
+        if (leader) {
+            bulk_wait_all();                      // every bulk store complete before the signal
+            if (pend_stage >= 0) mbar_arrive(&empty_bar[pend_stage]);
         }
     }
     complete(P);
@@ -454,8 +642,9 @@ __global__ void llrl_k_wait(unsigned long long *flag, unsigned long long target,
 
 }  // namespace
 
-// Cast-kernel variants (units in flight per thread, min resident CTAs per SM);
-// LLRL_CAST_VARIANT selects one for tuning, default kDefaultCastVariant.
+// Cast-kernel variants: 0-5 = register kernel llrl_k_cast<U, MINB> (units in
+// flight per thread, min resident CTAs per SM), 6 = TMA-staged llrl_k_cast_tma
+// (default).  LLRL_CAST_VARIANT selects one for tuning.
 struct CastVariant {
     const void *f32, *bf16;
 };
@@ -466,11 +655,14 @@ static const CastVariant kCastVariants[] = {LLRL_CV(4, 1), LLRL_CV(8, 1), LLRL_C
 constexpr int kNumCastVariants = int(sizeof(kCastVariants) / sizeof(kCastVariants[0]));
 
 static const void *kernel_for(int mode, int variant, bool src_f32) {
+    if (mode == 0 && variant == kCastTmaVariant)
+        return src_f32 ? (const void *)llrl_k_cast_tma<true> : (const void *)llrl_k_cast_tma<false>;
     if (mode == 1) {
         if (variant == 0) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
         return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false>;
     }
-    if (variant < 0 || variant >= kNumCastVariants) variant = kDefaultCastVariant;
+    if (variant < 0 || variant >= kNumCastVariants)   // the TMA variant, or out of range
+        return src_f32 ? (const void *)llrl_k_cast_tma<true> : (const void *)llrl_k_cast_tma<false>;
     return src_f32 ? kCastVariants[variant].f32 : kCastVariants[variant].bf16;
 }
 
@@ -478,6 +670,10 @@ static const void *kernel_for(int mode, int variant, bool src_f32) {
 static void launch_shape(int mode, int variant, bool src_f32, int *threads, size_t *smem) {
     *threads = kThreads;
     *smem = 0;
+    if (mode == 0 && variant == kCastTmaVariant) {
+        *threads = 32 + kCastWorkers;
+        *smem = size_t(kCastStages) * (kCastStageBytes + (src_f32 ? kCastStageBytes / 2 : 0));
+    }
     if (mode == 1 && variant != 0) {
         *threads = kThreads + 32;
         *smem = src_f32 ? size_t(fp8_stages<true>()) * fp8_stage_bytes<true>()
@@ -516,6 +712,6 @@ cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, threads, smem);
 }
 
-int num_cast_variants() { return kNumCastVariants; }
+int num_cast_variants() { return kNumCastVariants + 1; }   // + the TMA variant
 
 }  // namespace llrl

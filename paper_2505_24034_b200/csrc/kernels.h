@@ -13,6 +13,9 @@ namespace llrl {
 struct KParams {
     const Item *items;
     const Seg *segs;
+    const TmaRef *tma_refs;            // fp8 items: index i - fp8_base
+    const void *tmaps;                 // CUtensorMap array (global memory)
+    int fp8_base;
     unsigned long long *done;          // per (plan, device) CTA completion counter, or null
     unsigned long long done_target;    // epoch * gridDim.x of the signalling launch
     int item_begin, item_end;          // [begin, end) of this launch
@@ -22,7 +25,8 @@ struct KParams {
     void *dst[kMaxRanks];
 };
 
-constexpr int kDefaultCastVariant = 1;
+constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
+constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
 cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream);
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm);

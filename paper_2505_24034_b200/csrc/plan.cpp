@@ -7,7 +7,7 @@
 // src/dst offsets and leading dimensions).  Replicated trainer pieces (norms
 // under trainer TP) contribute one tile from one chosen holder (R5).  Tiles
 // become device work items:
-//   - bf16 / f32 destinations: K_CAST items of <= kChunk elements, executed by
+//   - bf16 / f32 destinations: K_CAST items of <= chunk_elems() elements, executed by
 //     the SOURCE GPU (push: cast before the transfer, so NVLink carries the
 //     destination width);
 //   - fp8 destinations: one item per 128x128 block of the generator-local
@@ -17,6 +17,7 @@
 // proportion to their bytes so that every NVLink peer and the local HBM copy
 // progress together.  The plan also records the traffic matrix and the
 // algorithmic HBM / NVLink bytes that bench.py's roofline uses.
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <numeric>
@@ -27,7 +28,16 @@ using namespace llrl;
 
 namespace {
 
-constexpr int64_t kChunk = 128 * 1024;   // elements per K_CAST item (256 KiB of bf16)
+// elements per K_CAST item (64 KiB of bf16: keeps the grid's working window small);
+// LLRL_CHUNK_ELEMS overrides (tuning knob)
+int64_t chunk_elems() {
+    static const int64_t c = [] {
+        const char *v = getenv("LLRL_CHUNK_ELEMS");
+        const int64_t x = v ? atoll(v) : 0;
+        return x >= 1024 ? x / 8 * 8 : int64_t(32 * 1024);
+    }();
+    return c;
+}
 
 struct Builder {
     const llrl_layout *S, *D;
@@ -109,10 +119,10 @@ struct Builder {
             // one 1-D run: scalar head up to a 16-byte destination boundary, vector body, scalar tail
             int64_t n = t.rows * t.cols, so = t.src_off, dof = t.dst_off;
             auto emit = [&](int64_t s, int64_t d, int64_t len, bool vec) {
-                for (int64_t i = 0; i < len; i += kChunk) {
+                for (int64_t i = 0; i < len; i += chunk_elems()) {
                     Item it = base;
                     it.src_off = s + i; it.dst_off = d + i;
-                    it.rows = 1; it.cols = int32_t(std::min(kChunk, len - i));
+                    it.rows = 1; it.cols = int32_t(std::min(chunk_elems(), len - i));
                     it.src_ld = it.cols; it.dst_ld = it.cols;
                     it.flags = uint16_t(fl | (vec ? F_VEC : 0));
                     out.push_back(it);
@@ -132,7 +142,7 @@ struct Builder {
         }
         const bool vec = (t.src_off % 8 == 0) && (t.dst_off % 8 == 0) && (t.cols % 8 == 0) &&
                          (t.src_ld % 8 == 0) && (t.dst_ld % 8 == 0);
-        const int64_t rows_per = std::max<int64_t>(1, kChunk / t.cols);
+        const int64_t rows_per = std::max<int64_t>(1, chunk_elems() / t.cols);
         for (int64_t r = 0; r < t.rows; r += rows_per) {
             Item it = base;
             it.rows = int32_t(std::min(rows_per, t.rows - r));
@@ -173,6 +183,39 @@ struct Builder {
         P->stats.src_bytes += src_bytes;
         P->stats.dst_bytes += dst_bytes;
         (void)exec;
+    }
+
+    // For every single-source vector fp8 block: the trainer piece it reads
+    // (one TMA tensor map per piece) and its coordinates inside the piece.
+    void make_tma_refs(DeviceWork &W) {
+        std::map<std::pair<int, int>, int> piece_map;   // (src rank, piece index) -> map index
+        W.tma_refs.assign(W.items.size() - size_t(W.n_cast), TmaRef{-1, 0, 0, 0});
+        for (size_t i = size_t(W.n_cast); i < W.items.size(); i++) {
+            const Item &it = W.items[i];
+            if (it.kind != K_FP8 || !(it.flags & F_VEC)) continue;
+            const auto &pcs = S->pieces[it.src_rank];
+            // the piece containing element src_off (pieces are in increasing offset order)
+            size_t lo = 0, hi = pcs.size();
+            while (hi - lo > 1) {
+                const size_t mid = (lo + hi) / 2;
+                if (pcs[mid].byte_off / es_src <= it.src_off) lo = mid; else hi = mid;
+            }
+            while (lo > 0 && pcs[lo].rows * pcs[lo].cols == 0) lo--;
+            const Piece &pc = pcs[lo];
+            const int64_t rel = it.src_off - pc.byte_off / es_src;
+            if ((pc.cols * es_src) % 16 != 0 || rel < 0 || rel >= pc.rows * pc.cols) continue;
+            auto key = std::make_pair(int(it.src_rank), int(lo));
+            auto f = piece_map.find(key);
+            int m;
+            if (f == piece_map.end()) {
+                m = int(W.tma_pieces.size());
+                piece_map[key] = m;
+                W.tma_pieces.push_back(TmaPiece{int(it.src_rank), pc.byte_off, pc.rows, pc.cols});
+            } else {
+                m = f->second;
+            }
+            W.tma_refs[i - size_t(W.n_cast)] = TmaRef{m, int32_t(rel % pc.cols), int32_t(rel / pc.cols), 0};
+        }
     }
 
     llrl_status make_items() {
@@ -310,6 +353,7 @@ struct Builder {
             W.fp8_off[size_t(n_groups)] = int64_t(W.items.size());
             for (int d = 0; d < G; d++)
                 if (sends[size_t(d)]) W.signal_devices.push_back(d);
+            make_tma_refs(W);
             P->stats.n_items += int64_t(W.items.size());
         }
         for (int e = 0; e < G; e++) {

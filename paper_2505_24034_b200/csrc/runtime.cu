@@ -51,6 +51,14 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         CK(cudaMalloc(&W.d_segs, W.segs.size() * sizeof(Seg)));
         CK(cudaMemcpy(W.d_segs, W.segs.data(), W.segs.size() * sizeof(Seg), cudaMemcpyHostToDevice));
     }
+    if (!W.tma_refs.empty()) {
+        CK(cudaMalloc(&W.d_tma_refs, W.tma_refs.size() * sizeof(TmaRef)));
+        CK(cudaMemcpy(W.d_tma_refs, W.tma_refs.data(), W.tma_refs.size() * sizeof(TmaRef), cudaMemcpyHostToDevice));
+    }
+    if (!W.tma_pieces.empty()) {
+        CK(cudaMalloc(&W.d_tmaps, W.tma_pieces.size() * 128));
+        W.h_tmaps.assign(W.tma_pieces.size() * 128, 0);
+    }
     CK(cudaMalloc(&W.d_done, 256));
     CK(cudaMemset(W.d_done, 0, 256));
     int sms = 0;
@@ -71,6 +79,44 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     }
     W.done_total = 0;
     W.uploaded_device = device;
+    return LLRL_OK;
+}
+
+typedef CUresult (*PFN_encode_tiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// (Re-)encode the device's TMA tensor maps when the trainer base pointers
+// change (first sync, or new buffers): one 2-D map per trainer piece read by
+// fp8 blocks, box 128x128 elements; uploaded on the sync stream.
+llrl_status ensure_tmaps(llrl_plan *p, DeviceWork &W, void *const *src_ptrs, cudaStream_t s) {
+    if (W.tma_pieces.empty()) return LLRL_OK;
+    bool same = W.tmap_src.size() == size_t(p->n_src);
+    for (int r = 0; same && r < p->n_src; r++) same = W.tmap_src[size_t(r)] == src_ptrs[r];
+    if (same) return LLRL_OK;
+    static PFN_encode_tiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) { set_error("cuTensorMapEncodeTiled unavailable"); return LLRL_E_CUDA; }
+        encode = reinterpret_cast<PFN_encode_tiled>(fn);
+    }
+    const int64_t es = dtype_bytes(p->src_dtype);
+    for (size_t m = 0; m < W.tma_pieces.size(); m++) {
+        const TmaPiece &tp = W.tma_pieces[m];
+        void *base = static_cast<char *>(src_ptrs[tp.src_rank]) + tp.byte_off;
+        const cuuint64_t dims[2] = {cuuint64_t(tp.cols), cuuint64_t(tp.rows)};
+        const cuuint64_t strides[1] = {cuuint64_t(tp.cols * es)};
+        const cuuint32_t box[2] = {128, 128}, estr[2] = {1, 1};
+        CUresult r = encode(reinterpret_cast<CUtensorMap *>(W.h_tmaps.data() + 128 * m),
+                            es == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d) for piece %zu", int(r), m); return LLRL_E_CUDA; }
+    }
+    CK(cudaMemcpyAsync(W.d_tmaps, W.h_tmaps.data(), W.h_tmaps.size(), cudaMemcpyHostToDevice, s));
+    W.tmap_src.assign(src_ptrs, src_ptrs + p->n_src);
     return LLRL_OK;
 }
 
@@ -126,6 +172,9 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
     if (st != LLRL_OK) return st;
     kp->items = W.d_items;
     kp->segs = W.d_segs;
+    kp->tma_refs = W.d_tma_refs;
+    kp->tmaps = W.d_tmaps;
+    kp->fp8_base = int(W.n_cast);
     return LLRL_OK;
 }
 
@@ -134,6 +183,10 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
 static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, KParams &kp, int64_t c0, int64_t c1,
                                  int64_t f0, int64_t f1, const std::vector<int> &sig, cudaStream_t s) {
     const bool has_fp8 = f1 > f0;
+    if (has_fp8 && W.fp8_variant == 1) {
+        llrl_status st = ensure_tmaps(p, W, const_cast<void *const *>(kp.src), s);
+        if (st != LLRL_OK) return st;
+    }
     for (int mode = 0; mode < 2; mode++) {
         const int64_t b = mode == 0 ? c0 : f0, e = mode == 0 ? c1 : f1;
         if (e <= b) continue;
@@ -290,6 +343,8 @@ void llrl_plan_destroy(llrl_plan *p) {
         cudaFree(W.d_items);
         cudaFree(W.d_segs);
         cudaFree(W.d_done);
+        cudaFree(W.d_tma_refs);
+        cudaFree(W.d_tmaps);
         for (void *e : W.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         if (W.h2d_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.h2d_stream));
         if (W.d2h_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.d2h_stream));
