@@ -264,7 +264,7 @@ def run_llrl(args):
     info = job.plan.device_info(job.device)
     kern = []
     if info.n_cast_items:
-        kern.append("llrl_k_cast (relayout + RNE cast, push)")
+        kern.append("llrl_k_cast_tma (TMA-staged relayout + RNE cast, push)")
     if info.n_fp8_items:
         kern.append("llrl_k_fp8_tma (fp8 block quant, TMA-staged)")
     roof["kernel"] = " + ".join(kern) + f"; whole sync of GPU {bdev} (binding), CUDA events on its stream"
