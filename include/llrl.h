@@ -95,6 +95,18 @@ typedef struct {
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
                                  llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
                                  llrl_layout **src_out, llrl_layout **dst_out);
+/* Same, with generator data parallelism (decoupled DP; reading R12):
+ * dp_gen replicas of the tp_gen-way generator, generator rank q = d*tp_gen + g
+ * holding exactly what TP rank g holds.  llrl_layout_describe == this with
+ * dp_gen = 1. */
+typedef struct {
+    int32_t fsdp, tp_train, tp_gen, dp_gen;
+    int32_t src_dtype, dst_dtype;   /* llrl_dtype */
+    uint32_t flags;
+    int32_t reserved;
+} llrl_layout_opts;
+llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts *opts,
+                                    llrl_layout **src_out, llrl_layout **dst_out);
 llrl_status llrl_layout_num_ranks(const llrl_layout *l, int *n);
 llrl_status llrl_layout_num_params(const llrl_layout *l, int *n);
 /* Bytes of rank `rank`'s flat buffer (a multiple of 256). */
@@ -153,7 +165,8 @@ typedef struct {
 llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
 
 /* ---- completion comm (a6) --------------------------------------------------
- * A comm owns one 256-byte flag buffer on `device` (epoch counters, R10).
+ * A comm owns one 256-byte flag buffer on `device`: word s counts arrivals
+ * from sender device s (cumulative), word 16 is set if a wait timed out (30 s).
  * Devices that exchange data in a plan must know each other's flag buffers:
  *   multi-process: llrl_comm_export on each, exchange the 64-byte handles
  *                  (e.g. torch.distributed.all_gather_object), llrl_comm_import;
@@ -166,6 +179,8 @@ llrl_status llrl_comm_export(const llrl_comm *c, void *handle64);
 llrl_status llrl_comm_import(llrl_comm *c, int peer_device, const void *handle64);
 llrl_status llrl_comm_flag_ptr(const llrl_comm *c, void **dev_ptr);
 llrl_status llrl_comm_set_peer(llrl_comm *c, int peer_device, void *peer_flag_dev_ptr);
+/* Synchronous check of the timeout flag (1 if any wait on this device gave up). */
+llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out);
 void llrl_comm_destroy(llrl_comm *c);
 
 /* ---- IPC helpers for caller-owned buffers ----------------------------------

@@ -19,7 +19,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED = 0, -1, -2, -3, -4
 E_NOMEM, E_UNCOVERED, E_OVERLAP = -7, -8, -9
-DTYPES = {"f32": 0, "bf16": 1, "fp8": 2}
+DTYPES = {"f32": 0, "bf16": 1, "fp8": 2, "mxfp8": 3}
 
 
 def build(force: bool = False) -> str:
@@ -38,7 +38,7 @@ class Model(ctypes.Structure):
 
 class Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("fsdp", "tp_train", "tp_gen", "src_dtype", "dst_dtype", "fsdp_inner")]
+                ("fsdp", "tp_train", "tp_gen", "src_dtype", "dst_dtype", "fsdp_inner", "dp_gen")]
 
 
 _lib = None
@@ -58,6 +58,7 @@ def lib():
         L.orc_e4m3_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.orc_fp8_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_mx_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_num_src_params.argtypes, L.orc_num_src_params.restype = [M], ctypes.c_int
         L.orc_num_dst_params.argtypes, L.orc_num_dst_params.restype = [M], ctypes.c_int
         L.orc_src_param_info.argtypes = [M, ctypes.c_int, i64p, i64p, ip]
@@ -101,15 +102,25 @@ def fp8_block(x: np.ndarray):
     return q, s[0]
 
 
+def mx_block(x: np.ndarray):
+    """Quantise one MXFP8 block (<= 32 elements) -> (uint8 codes, E8M0 scale byte)."""
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1)
+    q = np.empty(x.shape, dtype=np.uint8)
+    s = np.zeros(1, dtype=np.uint8)
+    lib().orc_mx_block(_ptr(x), x.size, _ptr(q), _ptr(s))
+    return q, int(s[0])
+
+
 class Layout:
     """The oracle's own view of both layouts for one configuration."""
 
-    def __init__(self, model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False):
+    def __init__(self, model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False,
+                 dp_gen=1):
         m = model
         self.m = Model(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ffn, m.vocab, m.with_embed)
-        self.c = Cfg(fsdp, tp_train, tp_gen, DTYPES[src_dtype], DTYPES[dst_dtype], int(fsdp_inner))
+        self.c = Cfg(fsdp, tp_train, tp_gen, DTYPES[src_dtype], DTYPES[dst_dtype], int(fsdp_inner), dp_gen)
         self.src_dtype, self.dst_dtype = src_dtype, dst_dtype
-        self.n_src, self.n_dst = fsdp * tp_train, tp_gen
+        self.n_src, self.n_dst = fsdp * tp_train, tp_gen * dp_gen
         L = lib()
         self.status = L.orc_check(ctypes.byref(self.m), ctypes.byref(self.c))
         self.n_src_params = L.orc_num_src_params(ctypes.byref(self.m))

@@ -45,7 +45,7 @@
 #define ORC_E_OVERLAP -9      /* a generator byte would be written twice */
 #define ORC_E_NOMEM -7
 
-enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2 };
+enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2, ORC_MXFP8 = 3 };
 
 typedef struct {
     int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, with_embed;
@@ -53,6 +53,7 @@ typedef struct {
 
 typedef struct {
     int32_t fsdp, tp_train, tp_gen, src_dtype, dst_dtype, fsdp_inner;
+    int32_t dp_gen;   /* generator data-parallel replicas (R12); rank q = d*tp_gen + g */
 } orc_cfg;
 
 /* ------------------------------------------------------------------------ */
@@ -82,6 +83,8 @@ uint16_t orc_bf16_rne(uint32_t b)
  * Written from the format definition: find the quantum of the binade of |v|
  * (2^(e-3) for normals, 2^-9 for subnormals), round |v|/quantum to the
  * nearest integer (ties to even) and encode the rounded value. */
+static uint8_t e4m3_encode(double a, uint8_t sign);
+
 uint8_t orc_e4m3_rn_satfinite(float v)
 {
     uint32_t vb;
@@ -89,7 +92,12 @@ uint8_t orc_e4m3_rn_satfinite(float v)
     uint8_t sign = (uint8_t)((vb >> 31) << 7);
     if (isnan(v))
         return (uint8_t)(sign | 0x7F);
-    double a = fabs((double)v);
+    return e4m3_encode(fabs((double)v), sign);
+}
+
+/* |value| a (exact, double) -> E4M3FN code, RN-even, saturating. */
+static uint8_t e4m3_encode(double a, uint8_t sign)
+{
     if (a == 0.0)
         return sign;
     if (a > 448.0)
@@ -119,6 +127,34 @@ uint8_t orc_e4m3_rn_satfinite(float v)
     int E = (e - 1) + 7;                         /* biased exponent */
     int m = (int)((f * 2.0 - 1.0) * 8.0);        /* exact: 3-bit mantissa */
     return (uint8_t)(sign | (uint8_t)(E << 3) | (uint8_t)m);
+}
+
+/* One MXFP8 block (OCP Microscaling Formats v1.0, E4M3 elements; DESIGN.md
+ * reading R13): n <= 32 consecutive elements of one row share the scale
+ * X = 2^(floor(log2(amax)) - emax_elem) with emax_elem = 8 (E4M3), the shared
+ * exponent clamped below at -127 (E8M0's smallest value; amax = 0 gives -127);
+ * each element is q = e4m3_rn_satfinite(v / X), the quotient taken exactly
+ * (one rounding).  The scale byte is the E8M0 code (shared exponent + 127). */
+void orc_mx_block(const float *x, int64_t n, uint8_t *q, uint8_t *scale)
+{
+    float amax = 0.0f;
+    for (int64_t i = 0; i < n; i++)
+        if (fabsf(x[i]) > amax)
+            amax = fabsf(x[i]);
+    int X = -127;
+    if (amax > 0.0f) {
+        int e;
+        frexp((double)amax, &e);                 /* amax = f * 2^e, f in [0.5, 1) */
+        X = (e - 1) - 8;                         /* floor(log2(amax)) - emax_elem */
+        if (X < -127)
+            X = -127;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        uint32_t vb;
+        memcpy(&vb, &x[i], 4);
+        q[i] = e4m3_encode(fabs(ldexp((double)x[i], -X)), (uint8_t)((vb >> 31) << 7));
+    }
+    *scale = (uint8_t)(X + 127);
 }
 
 /* Vectorised wrappers for the exhaustive pins. */
@@ -241,11 +277,11 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (m->n_layers < 0 || m->d_model <= 0 || m->n_heads <= 0 || m->n_kv_heads <= 0 ||
         m->head_dim <= 0 || m->d_ffn <= 0 || (m->with_embed && m->vocab <= 0))
         return ORC_E_INVALID;
-    if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0)
+    if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0 || c->dp_gen <= 0)
         return ORC_E_INVALID;
     if (c->src_dtype != ORC_F32 && c->src_dtype != ORC_BF16)
         return ORC_E_UNSUPPORTED;
-    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_FP8)
+    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_MXFP8)
         return ORC_E_UNSUPPORTED;
     if (c->dst_dtype == ORC_F32 && c->src_dtype != ORC_F32)
         return ORC_E_UNSUPPORTED;
@@ -416,12 +452,21 @@ static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int gp,
     default:
         return -1;
     }
-    if (c->dst_dtype != ORC_FP8)
+    if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8)
         *quant = 0;
     return n;
 }
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+/* Bytes of a quantised weight's scale grid (R9, R13): fp8 blocks: fp32
+ * [ceil(R/128), ceil(C/128)]; MXFP8: E8M0 bytes [R, ceil(C/32)]. */
+static int64_t scale_grid_bytes(const orc_cfg *c, int64_t R, int64_t C)
+{
+    if (c->dst_dtype == ORC_MXFP8)
+        return R * cdiv(C, 32);
+    return cdiv(R, 128) * cdiv(C, 128) * 4;
+}
 
 /* Byte offsets of generator param gp on rank g (R0, R9): params in canonical
  * order at 256-byte boundaries; a quantised weight's fp32 scale grid
@@ -430,6 +475,7 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
                   int64_t *rows, int64_t *cols, int *quant,
                   int64_t *byte_off, int64_t *scale_off)
 {
+    g %= c->tp_gen;   /* R12: replica d's rank d*T + g holds what TP rank g holds */
     int64_t off = 0;
     for (int q = 0; q <= gp; q++) {
         part_t parts[3];
@@ -444,7 +490,7 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
         if (qt) {
             off = align256(off);
             s_off = off;
-            off += cdiv(R, 128) * cdiv(C, 128) * 4;
+            off += scale_grid_bytes(c, R, C);
         }
         if (q == gp) {
             *rows = R; *cols = C; *quant = qt; *byte_off = data_off; *scale_off = s_off;
@@ -456,6 +502,7 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
 
 int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
 {
+    g %= c->tp_gen;
     int P = orc_num_dst_params(m);
     if (P == 0)
         return 0;
@@ -464,7 +511,7 @@ int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
     int64_t es = qt ? 1 : (c->dst_dtype == ORC_F32 ? 4 : 2);
     int64_t end = off + R * C * es;
     if (qt)
-        end = soff + cdiv(R, 128) * cdiv(C, 128) * 4;
+        end = soff + scale_grid_bytes(c, R, C);
     return align256(end);
 }
 
@@ -473,6 +520,7 @@ int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
 int orc_dst_element_source(const orc_model *m, const orc_cfg *c, int g, int gp,
                            int64_t lr, int64_t lc, int *src_param, int64_t *row, int64_t *col)
 {
+    g %= c->tp_gen;
     part_t parts[3];
     int64_t R, C; int qt;
     int n = dst_parts(m, c, g, gp, &R, &C, &qt, parts);
@@ -575,7 +623,16 @@ static int write_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
     }
     /* Step 3-4: cast and store */
     int rc = ORC_OK;
-    if (qt) {
+    if (qt && c->dst_dtype == ORC_MXFP8) {
+        int64_t nsc = cdiv(C, 32);
+        if ((rc = mark_written(written, off, R * C)) || (rc = mark_written(written, soff, R * nsc)))
+            goto out;
+        for (int64_t r = 0; r < R; r++)
+            for (int64_t j = 0; j < nsc; j++) {
+                int64_t n = C - j * 32 < 32 ? C - j * 32 : 32;
+                orc_mx_block(local + r * C + j * 32, n, dst + off + r * C + j * 32, dst + soff + r * nsc + j);
+            }
+    } else if (qt) {
         int64_t nbr = cdiv(R, 128), nbc = cdiv(C, 128);
         if ((rc = mark_written(written, off, R * C)) || (rc = mark_written(written, soff, nbr * nbc * 4)))
             goto out;
@@ -620,13 +677,13 @@ int orc_sync_range(const orc_model *m, const orc_cfg *c, const void *const *src,
     int rc = check_model(m, c);
     if (rc)
         return rc;
-    int P = orc_num_src_params(m), T = c->tp_gen;
+    int P = orc_num_src_params(m), T = c->tp_gen, ND = c->tp_gen * c->dp_gen;
     float **full = (float **)calloc((size_t)(P > 0 ? P : 1), sizeof(float *));
-    uint8_t **written = (uint8_t **)calloc((size_t)T, sizeof(uint8_t *));
+    uint8_t **written = (uint8_t **)calloc((size_t)ND, sizeof(uint8_t *));
     if (!full || !written) { free(full); free(written); return ORC_E_NOMEM; }
-    for (int g = 0; g < T; g++) {
-        written[g] = (uint8_t *)calloc((size_t)orc_dst_rank_bytes(m, c, g) + 1, 1);
-        if (!written[g]) { rc = ORC_E_NOMEM; goto done; }
+    for (int q = 0; q < ND; q++) {
+        written[q] = (uint8_t *)calloc((size_t)orc_dst_rank_bytes(m, c, q) + 1, 1);
+        if (!written[q]) { rc = ORC_E_NOMEM; goto done; }
     }
     for (int gp = gp_begin; gp < gp_end && rc == ORC_OK; gp++) {
         part_t parts[3];
@@ -635,8 +692,8 @@ int orc_sync_range(const orc_model *m, const orc_cfg *c, const void *const *src,
         for (int i = 0; i < n && rc == ORC_OK; i++)
             if (!full[parts[i].src_param])
                 rc = materialise(m, c, src, parts[i].src_param, &full[parts[i].src_param]);
-        for (int g = 0; g < T && rc == ORC_OK; g++)
-            rc = write_dst_param(m, c, g, gp, full, (uint8_t *)dst[g], written[g]);
+        for (int q = 0; q < ND && rc == ORC_OK; q++)   /* every replica gets its own copy */
+            rc = write_dst_param(m, c, q % T, gp, full, (uint8_t *)dst[q], written[q]);
         for (int i = 0; i < n; i++) {
             free(full[parts[i].src_param]);
             full[parts[i].src_param] = NULL;
@@ -645,8 +702,8 @@ int orc_sync_range(const orc_model *m, const orc_cfg *c, const void *const *src,
 done:
     for (int p = 0; p < P; p++)
         free(full[p]);
-    for (int g = 0; g < T; g++)
-        free(written[g]);
+    for (int q = 0; q < ND; q++)
+        free(written[q]);
     free(full);
     free(written);
     return rc;

@@ -73,7 +73,7 @@ struct DstParamDesc {
 struct llrl_layout {
     bool is_src;
     llrl_model model;
-    int fsdp, tp_train, tp_gen;
+    int fsdp, tp_train, tp_gen, dp_gen;
     int dtype;          // src: data dtype; dst: target dtype (F32/BF16/FP8)
     uint32_t flags;
     int n_ranks;
@@ -160,6 +160,8 @@ struct DeviceWork {
     std::vector<int64_t> cast_off, fp8_off;
     std::vector<std::vector<int>> group_signal;   // per group: devices written (excl. itself)
     std::vector<int> group_senders_in;            // per group: other devices writing here
+    std::vector<int> senders;                     // devices writing here (whole sync)
+    std::vector<std::vector<int>> group_senders;  // per group
     int64_t hbm_read = 0, hbm_write = 0, nvl_tx = 0, nvl_rx = 0;
     // device-side state (lazily created by the runtime)
     int uploaded_device = -1;
@@ -197,8 +199,8 @@ struct llrl_plan {
 
 struct llrl_comm {
     int device;
-    unsigned long long *flags = nullptr;   // [0]: arrivals into this device
+    unsigned long long *flags = nullptr;   // [s]: arrivals from sender device s; [kMaxDevices]: timeout flag
     unsigned long long *peer_flags[llrl::kMaxDevices] = {};
-    uint64_t expected = 0;                 // cumulative arrivals this device waits for
+    uint64_t expected[llrl::kMaxDevices] = {};   // cumulative arrivals expected from each sender
     bool ipc_opened[llrl::kMaxDevices] = {};
 };

@@ -622,18 +622,22 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
     complete(P);
 }
 
-// K3 receiver: spin (acquire, system scope) until `target` arrivals, bounded by
-// a timeout so a missing peer cannot hang the GPU; on timeout flag[1] = 1.
-__global__ void llrl_k_wait(unsigned long long *flag, unsigned long long target, unsigned long long timeout_ns) {
-    if (threadIdx.x != 0) return;
+// K3 receiver: lane s < kMaxDevices spins (acquire, system scope) until the
+// arrival counter of sender s reaches its target (0 = not a sender this time);
+// one counter per sender, so a fast sender's later arrivals can never stand in
+// for a slow sender's.  Bounded by a timeout so a missing peer cannot hang the
+// GPU; on timeout flag[kMaxDevices] = 1.
+__global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned long long timeout_ns) {
+    const int s = threadIdx.x;
+    if (s >= kMaxDevices || t.target[s] == 0) return;
     unsigned long long t0, now, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-        if (v >= target) return;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + s) : "memory");
+        if (v >= t.target[s]) return;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         if (now - t0 > timeout_ns) {
-            atomicExch(flag + 1, 1ULL);
+            atomicExch(flags + kMaxDevices, 1ULL);
             return;
         }
         __nanosleep(256);
@@ -695,8 +699,8 @@ cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, i
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
 }
 
-cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream) {
-    llrl_k_wait<<<1, 32, 0, stream>>>(flag, target, 30ull * 1000 * 1000 * 1000);
+cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream) {
+    llrl_k_wait<<<1, 32, 0, stream>>>(flags, t, 30ull * 1000 * 1000 * 1000);
     return cudaGetLastError();
 }
 

@@ -28,7 +28,10 @@ struct KParams {
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
 constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
-cudaError_t launch_wait(unsigned long long *flag, unsigned long long target, cudaStream_t stream);
+struct WaitTargets {
+    unsigned long long target[kMaxDevices];   // per sender device; 0 = do not wait
+};
+cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream);
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm);
 int num_cast_variants();
 int sync_threads();

@@ -203,6 +203,13 @@ llrl_status build_dst(llrl_layout *L) {
         }
         L->rank_bytes[g] = align_up(off);
     }
+    // R12: generator DP replicas -- rank d*T + g is laid out exactly like TP rank g
+    for (int d = 1; d < L->dp_gen; d++)
+        for (int g = 0; g < T; g++) {
+            L->pieces.push_back(L->pieces[size_t(g)]);
+            L->rank_bytes.push_back(L->rank_bytes[size_t(g)]);
+        }
+    L->n_ranks = T * L->dp_gen;
     return LLRL_OK;
 }
 
@@ -218,17 +225,18 @@ extern "C" {
 const char *llrl_last_error(void) { return llrl::g_err; }
 const char *llrl_version(void) { return "llrl 0.1 (sm_100a)"; }
 
-llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
-                                 llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
-                                 llrl_layout **src_out, llrl_layout **dst_out) {
-    if (!src_out || !dst_out || !model_ok(m) || fsdp <= 0 || tp_train <= 0 || tp_gen <= 0) {
+llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts *o, llrl_layout **src_out,
+                                    llrl_layout **dst_out) {
+    if (!o || !src_out || !dst_out || !model_ok(m) || o->fsdp <= 0 || o->tp_train <= 0 || o->tp_gen <= 0 ||
+        o->dp_gen <= 0) {
         set_error("llrl_layout_describe: invalid argument");
         return LLRL_E_INVALID;
     }
-    if (fsdp * tp_train > kMaxRanks || tp_gen > kMaxRanks) {
+    if (o->fsdp * o->tp_train > kMaxRanks || o->tp_gen * o->dp_gen > kMaxRanks) {
         set_error("llrl_layout_describe: at most %d ranks per side", kMaxRanks);
         return LLRL_E_INVALID;
     }
+    const int src_dtype = o->src_dtype, dst_dtype = o->dst_dtype;
     if ((src_dtype != LLRL_F32 && src_dtype != LLRL_BF16) ||
         (dst_dtype != LLRL_F32 && dst_dtype != LLRL_BF16 && dst_dtype != LLRL_FP8_E4M3) ||
         (dst_dtype == LLRL_F32 && src_dtype != LLRL_F32)) {
@@ -240,8 +248,8 @@ llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, in
     if (!S || !D) { delete S; delete D; set_error("out of host memory"); return LLRL_E_NOMEM; }
     for (llrl_layout *L : {S, D}) {
         L->model = *m;
-        L->fsdp = fsdp; L->tp_train = tp_train; L->tp_gen = tp_gen;
-        L->flags = flags;
+        L->fsdp = o->fsdp; L->tp_train = o->tp_train; L->tp_gen = o->tp_gen; L->dp_gen = o->dp_gen;
+        L->flags = o->flags;
         L->src_params = enumerate_src_params(*m);
     }
     S->is_src = true;  S->dtype = src_dtype;
@@ -256,6 +264,13 @@ llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, in
     }
     *src_out = S; *dst_out = D;
     return LLRL_OK;
+}
+
+llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
+                                 llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
+                                 llrl_layout **src_out, llrl_layout **dst_out) {
+    const llrl_layout_opts o{fsdp, tp_train, tp_gen, 1, src_dtype, dst_dtype, flags, 0};
+    return llrl_layout_describe_ex(m, &o, src_out, dst_out);
 }
 
 llrl_status llrl_layout_num_ranks(const llrl_layout *l, int *n) {

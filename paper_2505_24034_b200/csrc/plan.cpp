@@ -358,11 +358,20 @@ struct Builder {
         }
         for (int e = 0; e < G; e++) {
             P->dev[size_t(e)].group_senders_in.assign(size_t(n_groups), 0);
+            P->dev[size_t(e)].group_senders.assign(size_t(n_groups), {});
         }
         for (int e = 0; e < G; e++) {
-            for (int d : P->dev[size_t(e)].signal_devices) P->dev[size_t(d)].n_senders_in++;
+            for (int d : P->dev[size_t(e)].signal_devices) {
+                P->dev[size_t(d)].n_senders_in++;
+                P->dev[size_t(d)].senders.push_back(e);
+            }
             for (int grp = 0; grp < n_groups; grp++)
-                for (int d : P->dev[size_t(e)].group_signal[size_t(grp)]) P->dev[size_t(d)].group_senders_in[size_t(grp)]++;
+                for (int d : P->dev[size_t(e)].group_signal[size_t(grp)]) {
+                    P->dev[size_t(d)].group_senders_in[size_t(grp)]++;
+                    if (P->dev[size_t(d)].group_senders.empty())
+                        P->dev[size_t(d)].group_senders.assign(size_t(n_groups), {});
+                    P->dev[size_t(d)].group_senders[size_t(grp)].push_back(e);
+                }
         }
         // per-group byte ranges of every rank buffer (host <-> device streaming)
         P->src_group_range.assign(size_t(S->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));

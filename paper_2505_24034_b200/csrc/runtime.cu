@@ -64,7 +64,12 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const int64_t n_cast = W.n_cast, n_fp8 = int64_t(W.items.size()) - W.n_cast;
-    W.variant = kDefaultCastVariant;
+    // Cast kernel: TMA-staged (G->S->G bulk copies) when the device's work is
+    // HBM-bound; the register kernel (16-byte LDG/STG) when NVLink binds -- its
+    // peer stores measured ~3% faster than bulk stores over NVLink (profiles/).
+    const double t_hbm = double(W.hbm_read + W.hbm_write) / 6533.5e9;
+    const double t_nvl = double(std::max(W.nvl_tx, W.nvl_rx)) / 770e9;
+    W.variant = t_nvl > t_hbm ? 1 : kDefaultCastVariant;
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
@@ -201,17 +206,20 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
             kp.done = W.d_done;
             kp.done_target = W.done_total;
             kp.n_signal = int(sig.size());
-            for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]];
+            for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]] + comm->device;
         }
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
     }
     return LLRL_OK;
 }
 
-static llrl_status wait_arrivals(llrl_comm *comm, int n, cudaStream_t s) {
-    if (n <= 0) return LLRL_OK;
-    comm->expected += uint64_t(n);
-    CK(launch_wait(comm->flags, comm->expected, s));
+// One arrival is expected from every device in `senders` (per-sender counters).
+static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &senders, cudaStream_t s) {
+    if (senders.empty()) return LLRL_OK;
+    WaitTargets t;
+    std::memset(&t, 0, sizeof t);
+    for (int d : senders) t.target[d] = ++comm->expected[d];
+    CK(launch_wait(comm->flags, t, s));
     return LLRL_OK;
 }
 
@@ -225,7 +233,7 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     st = launch_ranges(p, W, comm, kp, 0, W.n_cast, W.n_cast, int64_t(W.items.size()), W.signal_devices, s);
     if (st != LLRL_OK) return st;
-    return wait_arrivals(comm, W.n_senders_in, s);
+    return wait_arrivals(comm, W.senders, s);
 }
 
 llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n) {
@@ -247,7 +255,7 @@ llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group
     st = launch_ranges(p, W, comm, kp, W.cast_off[g], W.cast_off[g + 1], W.fp8_off[g], W.fp8_off[g + 1],
                        W.group_signal[g], s);
     if (st != LLRL_OK) return st;
-    return wait_arrivals(comm, W.group_senders_in[g], s);
+    return wait_arrivals(comm, W.group_senders[g], s);
 }
 
 llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n) {
@@ -317,7 +325,7 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
         st = launch_ranges(p, W, comm, kp, W.cast_off[gg], W.cast_off[gg + 1], W.fp8_off[gg], W.fp8_off[gg + 1],
                            W.group_signal[gg], s);
         if (st != LLRL_OK) return st;
-        st = wait_arrivals(comm, W.group_senders_in[gg], s);
+        st = wait_arrivals(comm, W.group_senders[gg], s);
         if (st != LLRL_OK) return st;
         CK(cudaEventRecord(ev(size_t(2 * g + 1)), s));
         CK(cudaStreamWaitEvent(d2h, ev(size_t(2 * g + 1)), 0));
@@ -405,6 +413,15 @@ llrl_status llrl_comm_set_peer(llrl_comm *c, int peer_device, void *peer_flag_de
         else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
     }
     c->peer_flags[peer_device] = static_cast<unsigned long long *>(peer_flag_dev_ptr);
+    return LLRL_OK;
+}
+
+llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out) {
+    if (!c || !timed_out) { set_error("invalid argument"); return LLRL_E_INVALID; }
+    DeviceGuard guard(c->device);
+    unsigned long long v = 0;
+    CK(cudaMemcpy(&v, c->flags + kMaxDevices, sizeof v, cudaMemcpyDeviceToHost));
+    *timed_out = v != 0;
     return LLRL_OK;
 }
 

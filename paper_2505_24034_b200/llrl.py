@@ -27,11 +27,11 @@ MESH_FSDP_INNER = 1
  P_QKV, P_GATE_UP) = range(14)
 
 EXPORTS = [
-    "llrl_layout_describe", "llrl_layout_num_ranks", "llrl_layout_num_params", "llrl_layout_rank_bytes",
+    "llrl_layout_describe", "llrl_layout_describe_ex", "llrl_layout_num_ranks", "llrl_layout_num_params", "llrl_layout_rank_bytes",
     "llrl_layout_param_view", "llrl_layout_destroy", "llrl_plan_create", "llrl_plan_destroy",
     "llrl_plan_num_runs", "llrl_plan_get_runs", "llrl_plan_stats_get", "llrl_plan_traffic",
     "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
-    "llrl_comm_set_peer", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
+    "llrl_comm_set_peer", "llrl_comm_timed_out", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
     "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_last_error",
     "llrl_version",
 ]
@@ -46,6 +46,12 @@ class LlrlError(RuntimeError):
 class ModelDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab", "with_embed")]
+
+
+class LayoutOpts(ctypes.Structure):
+    _fields_ = [("fsdp", ctypes.c_int32), ("tp_train", ctypes.c_int32), ("tp_gen", ctypes.c_int32),
+                ("dp_gen", ctypes.c_int32), ("src_dtype", ctypes.c_int32), ("dst_dtype", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
 
 
 class ParamView(ctypes.Structure):
@@ -83,6 +89,7 @@ def _sig(name, args, res=ctypes.c_int):
 
 
 _sig("llrl_layout_describe", [_P(ModelDesc), _int, _int, _int, _int, _int, ctypes.c_uint32, _P(_vp), _P(_vp)])
+_sig("llrl_layout_describe_ex", [_P(ModelDesc), _P(LayoutOpts), _P(_vp), _P(_vp)])
 _sig("llrl_layout_num_ranks", [_vp, _P(_int)])
 _sig("llrl_layout_num_params", [_vp, _P(_int)])
 _sig("llrl_layout_rank_bytes", [_vp, _int, _P(_i64)])
@@ -101,6 +108,7 @@ _sig("llrl_comm_export", [_vp, ctypes.c_char_p])
 _sig("llrl_comm_import", [_vp, _int, ctypes.c_char_p])
 _sig("llrl_comm_flag_ptr", [_vp, _P(_vp)])
 _sig("llrl_comm_set_peer", [_vp, _int, _vp])
+_sig("llrl_comm_timed_out", [_vp, _P(_int)])
 _sig("llrl_comm_destroy", [_vp], None)
 _sig("llrl_ipc_handle", [_vp, ctypes.c_char_p, _P(_i64)])
 _sig("llrl_ipc_open", [ctypes.c_char_p, _i64, _P(_vp)])
@@ -163,13 +171,14 @@ class Layout:
     __del__ = close
 
 
-def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False):
-    """llrl_layout_describe -> (src Layout, dst Layout)."""
+def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False, dp_gen=1):
+    """llrl_layout_describe_ex -> (src Layout, dst Layout)."""
     m = ModelDesc(model.n_layers, model.d_model, model.n_heads, model.n_kv_heads, model.head_dim, model.d_ffn,
                   model.vocab, model.with_embed)
+    o = LayoutOpts(fsdp, tp_train, tp_gen, dp_gen, DTYPES[src_dtype], DTYPES[dst_dtype],
+                   MESH_FSDP_INNER if fsdp_inner else 0, 0)
     s, d = _vp(), _vp()
-    _check(_lib.llrl_layout_describe(ctypes.byref(m), fsdp, tp_train, tp_gen, DTYPES[src_dtype], DTYPES[dst_dtype],
-                                     MESH_FSDP_INNER if fsdp_inner else 0, ctypes.byref(s), ctypes.byref(d)))
+    _check(_lib.llrl_layout_describe_ex(ctypes.byref(m), ctypes.byref(o), ctypes.byref(s), ctypes.byref(d)))
     return Layout(s.value, True), Layout(d.value, False)
 
 
@@ -285,6 +294,11 @@ class Comm:
         p = _vp()
         _check(_lib.llrl_comm_flag_ptr(self._h, ctypes.byref(p)))
         return p.value
+
+    def timed_out(self) -> bool:
+        v = _int()
+        _check(_lib.llrl_comm_timed_out(self._h, ctypes.byref(v)))
+        return bool(v.value)
 
     def set_peer(self, peer_device, ptr):
         _check(_lib.llrl_comm_set_peer(self._h, peer_device, _vp(ptr)))

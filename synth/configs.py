@@ -48,6 +48,7 @@ class LayoutConfig:
     placement: str          # "disjoint" | "colocated" | "rotated"
     fsdp_inner: bool = False
     notes: str = ""
+    dp_gen: int = 1         # generator data-parallel replicas (R12)
 
     @property
     def n_src(self) -> int:
@@ -55,7 +56,7 @@ class LayoutConfig:
 
     @property
     def n_dst(self) -> int:
-        return self.tp_gen
+        return self.tp_gen * self.dp_gen
 
 
 CONFIGS = {
@@ -69,6 +70,10 @@ CONFIGS = {
                        notes="70B bf16 TP=8 -> fp8 TP=8 with 128x128 block scales"),
     "c5": LayoutConfig("c5", "llama3-405b-slice16", 2, 4, 8, "bf16", "bf16", "colocated",
                        notes="405B 16-layer slice FSDP=2xTP=4 -> TP=8, TP-innermost mesh"),
+    # NEXT f1: a generator pool of DP replicas, here the
+    # paper's best 8B setting "gen mp 1" with 4 replicas fed by a 4-GPU trainer.
+    "c6": LayoutConfig("c6", "llama3-8b", 4, 1, 1, "bf16", "bf16", "disjoint", dp_gen=4,
+                       notes="8B bf16 FSDP=4 (GPUs 0..G/2) -> bf16 TP=1 x DP=4 replicas (GPUs G/2..G)"),
 }
 
 

@@ -26,10 +26,10 @@ from synth import LayoutConfig  # noqa: E402
 from tests import harness  # noqa: E402
 
 
-def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2):
-    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner)
+def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2, dp=1):
+    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner, dp_gen=dp)
     job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False)
-    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner)
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner, dp)
     for rep in range(reps):
         src = harness.host_src(ol, seed + rep)
         for r, t in job.src.items():
@@ -72,6 +72,7 @@ def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, se
     want = harness.oracle_dst(ol, src, 0x5A)
     for g in job.dst:
         assert np.array_equal(hd[g].numpy(), want[g]), f"{cfg} sync_host: dst rank {g}"
+    assert job.comm is None or not job.comm.timed_out()
     job.close()
 
 
@@ -112,6 +113,8 @@ def main():
         toy_case(runner, world, *c)
         if dist.get_rank() == 0:
             print("ok", c, flush=True)
+    toy_case(runner, world, 4, 1, 1, "f32", "bf16", "disjoint", dp=4)      # generator DP replicas
+    toy_case(runner, world, 2, 2, 2, "bf16", "fp8", "disjoint", dp=2)
     if "--full" in sys.argv:
         for name in ("c2", "c3"):
             full_case(runner, world, name)

@@ -28,15 +28,16 @@ def rt():
     return llrl, runner
 
 
-def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None):
+def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None, dp=1):
     llrl, runner = rt
-    cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner)
+    cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner, dp_gen=dp)
     return runner.SyncJob(runner.JobSpec(cfg, 1, n_layers=n_layers), fill=False)
 
 
 def _run_and_compare(rt, job, seed, sentinel=0xA5, inject=None):
     cfg = job.cfg
-    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
+    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                       cfg.dp_gen)
     src = harness.host_src(ol, seed)
     if inject is not None:
         inject(ol, src)
@@ -117,6 +118,14 @@ def test_toy_parity_special_values(rt, sdt, ddt):
     # tp_train = 1: no replicated trainer pieces, so injected values stay consistent
     job = _toy_job(rt, "toy", 3, 1, 4, sdt, ddt)
     _run_and_compare(rt, job, seed=5, inject=_inject_specials)
+    job.close()
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,dp,sdt,ddt", [(4, 1, 1, 4, "f32", "bf16"), (2, 2, 2, 3, "bf16", "fp8")])
+def test_toy_parity_generator_dp(rt, fsdp, tpt, tpg, dp, sdt, ddt):
+    """Generator DP replicas (R12) filled from the same trainer shards."""
+    job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, dp=dp)
+    _run_and_compare(rt, job, seed=13)
     job.close()
 
 

@@ -120,6 +120,40 @@ def test_fp8_block_vs_numpy_ml_dtypes(oracle_lib, kind):
     assert np.array_equal(q, q_ref)
 
 
+@pytest.mark.parametrize("kind", ["random", "wide_range", "zero", "saturating", "subnormal", "partial"])
+def test_mx_block_vs_numpy_ml_dtypes(oracle_lib, kind):
+    """MXFP8 (R13): oracle vs numpy frexp / ml_dtypes; the scale byte decodes,
+    as ml_dtypes float8_e8m0fnu, to the power of two the block was divided by."""
+    rng = np.random.default_rng(11)
+    n = 32
+    if kind == "random":
+        x = rng.normal(0, 0.02, (64, n)).astype(np.float32)
+    elif kind == "wide_range":
+        x = (rng.normal(0, 1, (64, n)) * 10.0 ** rng.uniform(-37, 37, (64, 1))).astype(np.float32)
+    elif kind == "zero":
+        x = np.zeros((4, n), np.float32)
+        x[1, 3] = -0.0
+    elif kind == "saturating":   # amax mantissa >= 1.75: largest elements scale into (448, 512)
+        x = rng.uniform(-1, 1, (64, n)).astype(np.float32)
+        x[:, 0] = np.float32(1.96875)
+    elif kind == "subnormal":
+        x = (rng.normal(0, 1, (64, n)) * 1e-39).astype(np.float32)
+    else:
+        n = 20
+        x = rng.normal(0, 0.02, (8, n)).astype(np.float32)
+    qb, sb = brute.mx_quant(x)
+    for r in range(x.shape[0]):
+        q, sc = oracle.mx_block(x[r])
+        assert sc == sb[r, 0]
+        assert np.array_equal(q, qb[r])
+        amax = np.abs(x[r]).max()
+        scale = float(np.array([sc], np.uint8).view(ml_dtypes.float8_e8m0fnu).astype(np.float64)[0])
+        if amax > 0 and sc > 0:
+            assert 256 <= amax / scale < 512          # floor(log2 amax) - 8 == log2 scale
+    if kind == "saturating":
+        assert (qb[:, 0] & 0x7F == 0x7E).all()        # 1.96875 * 2^8 = 504 -> satfinite 448
+
+
 # --------------------------------------------------------------------------- layout / sync
 
 def _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src, sentinel=0):
@@ -157,11 +191,28 @@ def test_oracle_vs_brute_toy_sweep_bf16(oracle_lib, fsdp, tpt, tpg):
     (2, 4, 8, "bf16", "bf16", True),
     (3, 2, 4, "f32", "f32", False),       # identity cast (provenance mode)
     (4, 1, 1, "f32", "bf16", False),
+    (3, 1, 4, "f32", "mxfp8", False),     # MXFP8 (R13)
+    (2, 2, 8, "bf16", "mxfp8", True),
+    (1, 8, 8, "bf16", "mxfp8", False),
 ])
 def test_oracle_vs_brute_odd_layouts(oracle_lib, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]
     src, want = brute.build(m, 5, fsdp, tpt, tpg, sdt, ddt, inner)
     _, dst = _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src)
+    for d, w in zip(dst, want):
+        assert np.array_equal(d, w)
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,dp,sdt,ddt", [(4, 1, 1, 4, "f32", "bf16"), (2, 2, 2, 3, "bf16", "fp8"),
+                                                    (3, 1, 4, 2, "f32", "fp8")])
+def test_oracle_vs_brute_generator_dp(oracle_lib, fsdp, tpt, tpg, dp, sdt, ddt):
+    """Generator DP replicas (R12): every replica is a byte copy of its TP rank."""
+    m = MODELS["toy"]
+    src, want = brute.build(m, 6, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp)
+    L = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, False, dp)
+    assert L.status == 0 and L.n_dst == tpg * dp
+    dst = [np.zeros(L.dst_rank_bytes(q), np.uint8) for q in range(L.n_dst)]
+    assert L.sync(src, dst) == 0
     for d, w in zip(dst, want):
         assert np.array_equal(d, w)
 

@@ -58,6 +58,26 @@ def test_layout_matches_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner):
             assert (v.rows, v.cols, v.quantised, v.byte_off, v.scale_off) == O.dst_param(g, gp)
 
 
+@pytest.mark.parametrize("fsdp,tpt,tpg,dp,sdt,ddt,G", [(4, 1, 1, 4, "f32", "bf16", 8), (2, 2, 2, 3, "bf16", "fp8", 4),
+                                                      (3, 1, 4, 2, "f32", "fp8", 2)])
+def test_generator_dp_layout_and_plan(L, fsdp, tpt, tpg, dp, sdt, ddt, G):
+    m = MODELS["toy"]
+    S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp)
+    O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, False, dp)
+    assert D.n_ranks == tpg * dp
+    for q in range(D.n_ranks):
+        assert D.rank_bytes(q) == O.dst_rank_bytes(q)
+        for gp in range(D.n_params):
+            v = D.param_view(q, gp)
+            assert (v.rows, v.cols, v.quantised, v.byte_off, v.scale_off) == O.dst_param(q, gp)
+    ns, nd = fsdp * tpt, tpg * dp
+    plan = L.Plan(S, D, [r * G // (2 * ns) for r in range(ns)], [G // 2 + q * (G - G // 2) // nd for q in range(nd)])
+    src, want = brute.build(m, 8, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp)
+    got = _interpret(L, plan, D, src, sdt, ddt, [w.size for w in want])
+    for q in range(nd):
+        assert np.array_equal(got[q], want[q]), q
+
+
 def test_layout_errors(L):
     m = MODELS["toy"]
     for args, st in [((1, 1, 3), L.E_INDIVISIBLE), ((1, 1, 16), L.E_INDIVISIBLE), ((1, 3, 2), L.E_INDIVISIBLE),
