@@ -165,8 +165,10 @@ typedef struct {
 llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
 
 /* ---- completion comm (a6) --------------------------------------------------
- * A comm owns one 256-byte flag buffer on `device`: word s counts arrivals
- * from sender device s (cumulative), word 16 is set if a wait timed out (30 s).
+ * A comm owns one 512-byte flag buffer on `device`: word s counts data
+ * arrivals from sender device s, word 16 + s counts "trainer bytes staged"
+ * announcements of device s (llrl_sync_host with pull items), word 32 is set
+ * if a wait timed out (30 s).  All counters are cumulative.
  * Devices that exchange data in a plan must know each other's flag buffers:
  *   multi-process: llrl_comm_export on each, exchange the 64-byte handles
  *                  (e.g. torch.distributed.all_gather_object), llrl_comm_import;

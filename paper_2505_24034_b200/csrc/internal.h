@@ -162,6 +162,10 @@ struct DeviceWork {
     std::vector<int> group_senders_in;            // per group: other devices writing here
     std::vector<int> senders;                     // devices writing here (whole sync)
     std::vector<std::vector<int>> group_senders;  // per group
+    // pull items (multi-source fp8 blocks) read peers' trainer buffers: in
+    // llrl_sync_host those peers announce "group g staged" (src-ready counters)
+    std::vector<std::vector<int>> pull_from;      // per group: devices this device reads from
+    std::vector<std::vector<int>> pull_to;        // per group: devices that read from this device
     int64_t hbm_read = 0, hbm_write = 0, nvl_tx = 0, nvl_rx = 0;
     // device-side state (lazily created by the runtime)
     int uploaded_device = -1;
@@ -199,8 +203,11 @@ struct llrl_plan {
 
 struct llrl_comm {
     int device;
-    unsigned long long *flags = nullptr;   // [s]: arrivals from sender device s; [kMaxDevices]: timeout flag
+    // flags[s]: data arrivals from sender device s; flags[kMaxDevices + s]:
+    // "trainer bytes staged" announcements from device s (llrl_sync_host);
+    // flags[2 * kMaxDevices]: wait-timeout flag.  512 bytes.
+    unsigned long long *flags = nullptr;
     unsigned long long *peer_flags[llrl::kMaxDevices] = {};
-    uint64_t expected[llrl::kMaxDevices] = {};   // cumulative arrivals expected from each sender
+    uint64_t expected[2 * llrl::kMaxDevices] = {};   // cumulative arrivals expected per slot
     bool ipc_opened[llrl::kMaxDevices] = {};
 };

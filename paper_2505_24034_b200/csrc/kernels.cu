@@ -622,14 +622,15 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
     complete(P);
 }
 
-// K3 receiver: lane s < kMaxDevices spins (acquire, system scope) until the
-// arrival counter of sender s reaches its target (0 = not a sender this time);
-// one counter per sender, so a fast sender's later arrivals can never stand in
-// for a slow sender's.  Bounded by a timeout so a missing peer cannot hang the
-// GPU; on timeout flag[kMaxDevices] = 1.
+// K3 receiver: lane s spins (acquire, system scope) until flag slot s reaches
+// its target (0 = not waited on): slots 0..15 count data arrivals per sender
+// device, 16..31 "trainer bytes staged" announcements per device.  One counter
+// per sender, so a fast sender's later arrivals can never stand in for a slow
+// sender's.  Bounded by a timeout so a missing peer cannot hang the GPU; on
+// timeout flag[2 * kMaxDevices] = 1.
 __global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned long long timeout_ns) {
     const int s = threadIdx.x;
-    if (s >= kMaxDevices || t.target[s] == 0) return;
+    if (s >= 2 * kMaxDevices || t.target[s] == 0) return;
     unsigned long long t0, now, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
@@ -637,11 +638,19 @@ __global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned l
         if (v >= t.target[s]) return;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         if (now - t0 > timeout_ns) {
-            atomicExch(flags + kMaxDevices, 1ULL);
+            atomicExch(flags + 2 * kMaxDevices, 1ULL);
             return;
         }
         __nanosleep(256);
     }
+}
+
+// Announce (release, system scope) that everything ordered before this kernel
+// on its stream -- e.g. the H2D copy of a layer group -- is visible.
+__global__ void llrl_k_signal(SignalTargets t) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    for (int i = 0; i < t.n; i++) asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(t.slot[i]) : "memory");
 }
 
 }  // namespace
@@ -697,6 +706,11 @@ cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, i
     launch_shape(mode, variant, src_f32, &threads, &smem);
     void *args[] = {const_cast<KParams *>(&P)};
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
+}
+
+cudaError_t launch_signal(const SignalTargets &t, cudaStream_t stream) {
+    llrl_k_signal<<<1, 32, 0, stream>>>(t);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream) {

@@ -29,8 +29,13 @@ constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
 constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
 struct WaitTargets {
-    unsigned long long target[kMaxDevices];   // per sender device; 0 = do not wait
+    unsigned long long target[2 * kMaxDevices];   // per flag slot; 0 = do not wait
 };
+struct SignalTargets {
+    unsigned long long *slot[kMaxDevices];
+    int n;
+};
+cudaError_t launch_signal(const SignalTargets &t, cudaStream_t stream);
 cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream);
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm);
 int num_cast_variants();

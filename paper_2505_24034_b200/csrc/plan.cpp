@@ -373,6 +373,30 @@ struct Builder {
                     P->dev[size_t(d)].group_senders[size_t(grp)].push_back(e);
                 }
         }
+        // pull dependencies per group (multi-source fp8 blocks read peers' trainer bytes)
+        for (int e = 0; e < G; e++) {
+            P->dev[size_t(e)].pull_from.assign(size_t(n_groups), {});
+            P->dev[size_t(e)].pull_to.assign(size_t(n_groups), {});
+        }
+        for (int e = 0; e < G; e++) {
+            DeviceWork &W = P->dev[size_t(e)];
+            for (int grp = 0; grp < n_groups; grp++) {
+                std::vector<char> from(size_t(G), 0);
+                for (int64_t i = W.fp8_off[size_t(grp)]; i < W.fp8_off[size_t(grp) + 1]; i++) {
+                    const Item &it = W.items[size_t(i)];
+                    if (it.kind != K_FP8_MULTI) continue;
+                    for (int k = 0; k < it.src_rank; k++) {
+                        const int sd = P->src_device[size_t(W.segs[size_t(it.src_off) + size_t(k)].src_rank)];
+                        if (sd != e) from[size_t(sd)] = 1;
+                    }
+                }
+                for (int sd = 0; sd < G; sd++)
+                    if (from[size_t(sd)]) {
+                        W.pull_from[size_t(grp)].push_back(sd);
+                        P->dev[size_t(sd)].pull_to[size_t(grp)].push_back(e);
+                    }
+            }
+        }
         // per-group byte ranges of every rank buffer (host <-> device streaming)
         P->src_group_range.assign(size_t(S->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));
         P->dst_group_range.assign(size_t(D->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));

@@ -150,7 +150,8 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
         return LLRL_E_INVALID;
     }
     DeviceWork &W = p->dev[size_t(device)];
-    const bool cross = !W.signal_devices.empty() || W.n_senders_in > 0;
+    bool cross = !W.signal_devices.empty() || W.n_senders_in > 0;
+    for (size_t g = 0; g < W.pull_from.size(); g++) cross = cross || !W.pull_from[g].empty() || !W.pull_to[g].empty();
     if (cross) {
         if (!comm || comm->device != device) {
             set_error("llrl_sync: device %d exchanges data with peers and needs its comm", device);
@@ -213,12 +214,12 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
     return LLRL_OK;
 }
 
-// One arrival is expected from every device in `senders` (per-sender counters).
-static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &senders, cudaStream_t s) {
-    if (senders.empty()) return LLRL_OK;
+// One arrival is expected in slot base + d for every device d in `devs`.
+static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &devs, cudaStream_t s, int base = 0) {
+    if (devs.empty()) return LLRL_OK;
     WaitTargets t;
     std::memset(&t, 0, sizeof t);
-    for (int d : senders) t.target[d] = ++comm->expected[d];
+    for (int d : devs) t.target[base + d] = ++comm->expected[base + d];
     CK(launch_wait(comm->flags, t, s));
     return LLRL_OK;
 }
@@ -319,9 +320,20 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
                                static_cast<const char *>(host_src[r]) + rg.first, size_t(rg.second - rg.first),
                                cudaMemcpyHostToDevice, h2d));
         }
+        const size_t gg = size_t(g);
+        if (!W.pull_to[gg].empty()) {            // peers pull this group's trainer bytes
+            SignalTargets t;
+            std::memset(&t, 0, sizeof t);
+            for (int d : W.pull_to[gg]) {
+                if (!comm || !comm->peer_flags[d]) { set_error("llrl_sync_host: no flag mapping for %d", d); return LLRL_E_NOPEER; }
+                t.slot[t.n++] = comm->peer_flags[d] + kMaxDevices + device;
+            }
+            CK(launch_signal(t, h2d));
+        }
         CK(cudaEventRecord(ev(size_t(2 * g)), h2d));
         CK(cudaStreamWaitEvent(s, ev(size_t(2 * g)), 0));
-        const size_t gg = size_t(g);
+        st = wait_arrivals(comm, W.pull_from[gg], s, kMaxDevices);   // their bytes staged
+        if (st != LLRL_OK) return st;
         st = launch_ranges(p, W, comm, kp, W.cast_off[gg], W.cast_off[gg + 1], W.fp8_off[gg], W.fp8_off[gg + 1],
                            W.group_signal[gg], s);
         if (st != LLRL_OK) return st;
@@ -368,8 +380,8 @@ llrl_status llrl_comm_create(int device, llrl_comm **out) {
     if (!c) { set_error("out of host memory"); return LLRL_E_NOMEM; }
     c->device = device;
     DeviceGuard guard(device);
-    cudaError_t e = cudaMalloc(&c->flags, 256);
-    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, 256);
+    cudaError_t e = cudaMalloc(&c->flags, 512);
+    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, 512);
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "llrl_comm_create"); }
     c->peer_flags[device] = c->flags;
     *out = c;
@@ -420,7 +432,7 @@ llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out) {
     if (!c || !timed_out) { set_error("invalid argument"); return LLRL_E_INVALID; }
     DeviceGuard guard(c->device);
     unsigned long long v = 0;
-    CK(cudaMemcpy(&v, c->flags + kMaxDevices, sizeof v, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v, c->flags + 2 * kMaxDevices, sizeof v, cudaMemcpyDeviceToHost));
     *timed_out = v != 0;
     return LLRL_OK;
 }
