@@ -50,7 +50,10 @@ typedef enum {
     LLRL_E_NOMEM = -7         /* host or device allocation failed            */
 } llrl_status;
 
-typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2 } llrl_dtype;
+/* LLRL_MXFP8: OCP MX E4M3 elements with one E8M0 scale byte per 1x32 row
+ * group (NEXT f2, "quantization (fp8 or fp4) on the inference side", P:145;
+ * reading R13); scale grid [R, ceil(C/32)] bytes after each quantised weight. */
+typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3 } llrl_dtype;
 
 /* Llama-style decoder shapes (Llama-3.1 config.json fields [ext]). */
 typedef struct {
@@ -76,7 +79,7 @@ typedef struct {
     int32_t kind;        /* LLRL_P_* */
     int32_t layer;       /* -1 for embed / final_norm / lm_head */
     int32_t dtype;       /* llrl_dtype of the data */
-    int32_t quantised;   /* 1: fp8 data followed by an fp32 scale grid (R7, R9) */
+    int32_t quantised;   /* 1: fp8 data followed by its scale grid (R7, R9, R13) */
     int64_t rows, cols;  /* local shape, row-major, leading dimension = cols */
     int64_t byte_off;    /* data offset in the rank buffer */
     int64_t scale_off;   /* scale grid offset, -1 if not quantised */
@@ -89,7 +92,7 @@ typedef struct {
  * Describe the trainer (src) and generator (dst) layouts of `m` for a trainer
  * mesh fsdp x tp_train (fsdp*tp_train ranks, R1-R3) and a generator with
  * tp_gen ranks (R4).  src_dtype in {F32, BF16}; dst_dtype in {F32 (only from
- * F32: identity/provenance mode), BF16, FP8_E4M3 (R7)}.
+ * F32: identity/provenance mode), BF16, FP8_E4M3 (R7), MXFP8 (R13)}.
  * Errors: INVALID (NULL, non-positive sizes), INDIVISIBLE, UNSUPPORTED.
  * Ownership: *src_out and *dst_out belong to the caller (llrl_layout_destroy). */
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,

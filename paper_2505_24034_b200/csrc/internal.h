@@ -17,9 +17,11 @@ constexpr int kMaxRanks = 64;      // per side; kernel parameter tables are size
 constexpr int kMaxDevices = 16;
 constexpr int64_t kAlign = 256;    // R0: every piece starts at a 256-byte boundary
 constexpr int kFp8Block = 128;     // R7
+constexpr int kMxGroup = 32;       // R13
 
 void set_error(const char *fmt, ...);
 int64_t dtype_bytes(int dt);
+int64_t scale_grid_bytes(int dt, int64_t rows, int64_t cols);
 
 // A rectangle [r0, r1) x [c0, c1) of a full parameter tensor.
 struct Rect {
@@ -100,6 +102,7 @@ enum ItemKind : uint16_t {
 enum ItemFlag : uint16_t {
     F_VEC = 1,         // 16-byte vector path legal (offsets / lds / cols aligned)
     F_DST_F32 = 2,     // destination dtype f32 (identity), else bf16 (K_CAST)
+    F_MX = 4,          // K_CAST into MXFP8 codes (1 byte); aux = scale byte base (R13)
 };
 
 // Device work item (48 bytes).  Offsets in elements of each side's dtype, except

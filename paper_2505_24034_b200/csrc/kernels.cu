@@ -513,7 +513,7 @@ template <bool SRC_F32>
 __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {
     constexpr int es = SRC_F32 ? 4 : 2;
     extern __shared__ __align__(128) unsigned char stages[];   // kCastStages x (in 32 KiB [+ out 16 KiB])
-    constexpr int kOut = SRC_F32 ? kCastStageBytes / 2 : 0;
+    constexpr int kOut = kCastStageBytes / 2;   // bf16 or MXFP8 codes of a chunk
     constexpr int kStride = kCastStageBytes + kOut;
     __shared__ __align__(8) uint64_t full_bar[kCastStages], empty_bar[kCastStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -582,8 +582,9 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
             }
             int rows_per, segs;
             const int nch = cast_chunks(it, es, &rows_per, &segs);
-            const bool cast = SRC_F32 && !dst_f32;
-            const int des = cast ? 2 : es;
+            const bool mx = it.flags & F_MX;
+            const bool cast = SRC_F32 && !dst_f32 && !mx;
+            const int des = mx ? 1 : cast ? 2 : es;
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&full_bar[st], (n / kCastStages) & 1);
@@ -598,6 +599,36 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
                         reinterpret_cast<uint2 *>(out)[u] =
                             make_uint2(bf16x2_rn(__uint_as_float(a.x), __uint_as_float(a.y)),
                                        bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    cast_workers_sync();
+                } else if (mx) {
+                    // MXFP8 (R13): lanes (2j, 2j+1) hold the two halves of one 1x32 group
+                    out = in + kCastStageBytes;
+                    const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
+                    for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
+                        const int u = u0 + wt;
+                        const bool live = u < nunits;
+                        constexpr int W = SRC_F32 ? 4 : 2;
+                        uint4 w[W];
+                        uint32_t amax = 0;
+#pragma unroll
+                        for (int j = 0; j < W; j++) {
+                            w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
+                            amax = word_amax<SRC_F32>(w[j], amax);
+                        }
+                        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+                        // shared exponent floor(log2 amax) - 8, clamped at -127: E8M0 code max(E - 8, 0)
+                        const int code = max(int(amax >> 23) - 8, 0);
+                        const float inv = __uint_as_float(uint32_t(254 - code) << 23);   // 2^-(code - 127)
+                        if (live) {
+                            reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
+                            if ((u & 1) == 0) {
+                                const int e0 = u * 16, r = e0 / c.nc, cc = e0 - r * c.nc;
+                                const int64_t o = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0 + cc;
+                                dbase[it.aux + o / kMxGroup] = static_cast<char>(code);
+                            }
+                        }
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     cast_workers_sync();
@@ -685,7 +716,7 @@ static void launch_shape(int mode, int variant, bool src_f32, int *threads, size
     *smem = 0;
     if (mode == 0 && variant == kCastTmaVariant) {
         *threads = 32 + kCastWorkers;
-        *smem = size_t(kCastStages) * (kCastStageBytes + (src_f32 ? kCastStageBytes / 2 : 0));
+        *smem = size_t(kCastStages) * (kCastStageBytes + kCastStageBytes / 2);
     }
     if (mode == 1 && variant != 0) {
         *threads = kThreads + 32;

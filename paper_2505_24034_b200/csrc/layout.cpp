@@ -25,6 +25,12 @@ void set_error(const char *fmt, ...) {
 
 int64_t dtype_bytes(int dt) { return dt == LLRL_F32 ? 4 : dt == LLRL_BF16 ? 2 : 1; }
 
+// R9 / R13: fp8 blocks -> fp32 [ceil(R/128), ceil(C/128)]; MXFP8 -> E8M0 bytes [R, ceil(C/32)].
+int64_t scale_grid_bytes(int dt, int64_t rows, int64_t cols) {
+    if (dt == LLRL_MXFP8) return rows * ((cols + kMxGroup - 1) / kMxGroup);
+    return ((rows + kFp8Block - 1) / kFp8Block) * ((cols + kFp8Block - 1) / kFp8Block) * 4;
+}
+
 static int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // R0: canonical source-parameter list.
@@ -189,15 +195,15 @@ llrl_status build_dst(llrl_layout *L) {
                 return LLRL_E_INVALID;
             }
             pc.rect = Rect{0, pc.rows, 0, pc.cols};
-            pc.quantised = L->dtype == LLRL_FP8_E4M3 && dp[i].quantisable;
-            pc.dtype = pc.quantised ? LLRL_FP8_E4M3 : (L->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
+            pc.quantised = (L->dtype == LLRL_FP8_E4M3 || L->dtype == LLRL_MXFP8) && dp[i].quantisable;
+            pc.dtype = pc.quantised ? L->dtype : (L->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
             off = align_up(off);
             pc.byte_off = off;
             off += pc.rows * pc.cols * dtype_bytes(pc.dtype);
             if (pc.quantised) {
                 off = align_up(off);
                 pc.scale_off = off;
-                off += ((pc.rows + kFp8Block - 1) / kFp8Block) * ((pc.cols + kFp8Block - 1) / kFp8Block) * 4;
+                off += scale_grid_bytes(L->dtype, pc.rows, pc.cols);
             }
             L->pieces[g].push_back(pc);
         }
@@ -238,7 +244,7 @@ llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts 
     }
     const int src_dtype = o->src_dtype, dst_dtype = o->dst_dtype;
     if ((src_dtype != LLRL_F32 && src_dtype != LLRL_BF16) ||
-        (dst_dtype != LLRL_F32 && dst_dtype != LLRL_BF16 && dst_dtype != LLRL_FP8_E4M3) ||
+        (dst_dtype != LLRL_F32 && dst_dtype != LLRL_BF16 && dst_dtype != LLRL_FP8_E4M3 && dst_dtype != LLRL_MXFP8) ||
         (dst_dtype == LLRL_F32 && src_dtype != LLRL_F32)) {
         set_error("llrl_layout_describe: unsupported dtypes src=%d dst=%d", src_dtype, dst_dtype);
         return LLRL_E_UNSUPPORTED;

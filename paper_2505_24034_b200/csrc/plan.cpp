@@ -156,6 +156,39 @@ struct Builder {
         }
     }
 
+    // MXFP8 tile -> cast items with F_MX.  Every 1x32 group must lie inside one
+    // tile and one item: the tile's columns (or, for a run contiguous on both
+    // sides, its whole length) start and end on 32-element group boundaries.
+    llrl_status add_mx_items(const Tile &t) {
+        const Piece &pc = D->pieces[size_t(t.dst_rank)][size_t(t.dst_param)];
+        const int64_t base = pc.byte_off;                 // codes are bytes: element == byte
+        const bool contiguous = t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld);
+        const bool ok = (t.dst_off - base) % kMxGroup == 0 && (contiguous ? (t.rows * t.cols) % kMxGroup == 0
+                                                                          : t.cols % kMxGroup == 0) &&
+                        t.src_off % 8 == 0 && t.src_ld % 8 == 0 && pc.cols % kMxGroup == 0;
+        if (!ok) {
+            set_error("MXFP8: tile of generator param %d is not aligned to 1x32 groups", t.dst_param);
+            return LLRL_E_UNSUPPORTED;
+        }
+        std::vector<Item> tmp;
+        add_cast_items(t, tmp);
+        const int sd = P->src_device[size_t(t.src_rank)], dd = P->dst_device[size_t(t.dst_rank)];
+        const SrcParam &sp = S->src_params[size_t(t.src_param)];
+        auto &L = lists[size_t(sd)][size_t(dd)][size_t(group_of(sp.kind, sp.layer))];
+        for (Item it : tmp) {
+            it.flags = uint16_t((it.flags & F_VEC) | F_MX);
+            if (!(it.flags & F_VEC) || it.dst_off % kMxGroup != 0) {
+                set_error("MXFP8: unaligned cast item");
+                return LLRL_E_UNSUPPORTED;
+            }
+            it.aux = pc.scale_off - base / kMxGroup;      // scale byte of element o: aux + o / 32
+            L.push_back(it);
+        }
+        const int64_t n = t.rows * t.cols;
+        account(sd, sd, dd, n * es_src, n + n / kMxGroup, false);
+        return LLRL_OK;
+    }
+
     // work lists per executing device, per destination device, per layer group
     std::vector<std::vector<std::vector<std::vector<Item>>>> lists;   // [exec dev][dst dev][group]
     std::vector<std::vector<Seg>> seglists;                           // [exec dev] (pull blocks)
@@ -224,9 +257,15 @@ struct Builder {
         P->n_groups = n_groups;
         lists.assign(G, std::vector<std::vector<std::vector<Item>>>(G, std::vector<std::vector<Item>>(n_groups)));
         seglists.assign(G, {});
-        // bf16 / f32 tiles
+        // bf16 / f32 tiles, and MXFP8 tiles (row-wise 1x32 groups ride on cast items, R13)
+        const bool mx = D->dtype == LLRL_MXFP8;
         for (const Tile &t : P->tiles) {
-            if (t.quant) continue;
+            if (t.quant && !mx) continue;
+            if (t.quant) {
+                llrl_status st = add_mx_items(t);
+                if (st != LLRL_OK) return st;
+                continue;
+            }
             const int sd = P->src_device[t.src_rank], dd = P->dst_device[t.dst_rank];
             const SrcParam &sp = S->src_params[size_t(t.src_param)];
             add_cast_items(t, lists[sd][dd][size_t(group_of(sp.kind, sp.layer))]);

@@ -71,6 +71,8 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     const double t_nvl = double(std::max(W.nvl_tx, W.nvl_rx)) / 770e9;
     W.variant = t_nvl > t_hbm ? 1 : kDefaultCastVariant;
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
+    for (const Item &it : W.items)
+        if (it.flags & F_MX) { W.variant = kCastTmaVariant; break; }        // MXFP8 lives in the TMA kernel only
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
     if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = atoi(v) ? 1 : 0;

@@ -74,6 +74,9 @@ CONFIGS = {
     # paper's best 8B setting "gen mp 1" with 4 replicas fed by a 4-GPU trainer.
     "c6": LayoutConfig("c6", "llama3-8b", 4, 1, 1, "bf16", "bf16", "disjoint", dp_gen=4,
                        notes="8B bf16 FSDP=4 (GPUs 0..G/2) -> bf16 TP=1 x DP=4 replicas (GPUs G/2..G)"),
+    # NEXT f2: MX formats for the generator, as tcgen05 block-scaled MMA consumes them
+    "c7": LayoutConfig("c7", "llama3-70b", 1, 8, 8, "bf16", "mxfp8", "colocated",
+                       notes="70B bf16 TP=8 -> MXFP8 TP=8 (E4M3 + E8M0 per 1x32)"),
 }
 
 

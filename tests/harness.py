@@ -89,3 +89,17 @@ def expected_fp8_block_fast(ol: oracle.Layout, seed, g, gp, bi, bj):
             bits = bits << np.uint32(16)
         x[i] = bits.view(np.float32)
     return oracle.fp8_block(x)
+
+
+def expected_mx_group(ol: oracle.Layout, seed, g, gp, r, j):
+    """(codes, E8M0 byte) of MXFP8 group j of row r of generator param gp, from the oracle."""
+    R, C, q, off, soff = ol.dst_param(g, gp)
+    c0 = j * 32
+    n = min(32, C - c0)
+    p, row, col = ol.dst_element_source(g, gp, r, c0)
+    assert ol.dst_element_source(g, gp, r, c0 + n - 1) == (p, row, col + n - 1)
+    is_norm = ol.src_param_info(p)[2] == 2
+    bits = synth.weight_bits(seed, p, is_norm, ol.src_dtype, np.array([row]), np.arange(col, col + n)).astype(np.uint32)
+    if ol.src_dtype == "bf16":
+        bits = bits << np.uint32(16)
+    return oracle.mx_block(bits.view(np.float32))

@@ -108,6 +108,7 @@ def main():
         (3, 1, 4, "f32", "fp8", "colocated"),     # pull (multi-source) fp8 blocks across GPUs
         (2, 2, 8, "bf16", "fp8", "rotated"),
         (3, 2, 4, "f32", "f32", "disjoint"),
+        (2, 2, 8, "bf16", "mxfp8", "rotated"),
     ]
     for c in cases:
         toy_case(runner, world, *c)

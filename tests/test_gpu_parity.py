@@ -69,7 +69,7 @@ def test_fill_matches_synth(rt):
 
 
 SWEEP = [(f, tt, tg, sdt, ddt) for f in (1, 2, 3, 8) for tt in (1, 2, 4) for tg in (1, 2, 4, 8)
-         for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"))]
+         for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp8"))]
 
 
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", SWEEP)
@@ -86,6 +86,8 @@ def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
     (3, 2, 4, "f32", "f32", False),     # identity (provenance mode)
     (8, 4, 8, "bf16", "bf16", False),   # 32 trainer ranks
     (1, 8, 8, "f32", "fp8", False),
+    (3, 1, 4, "f32", "mxfp8", False),   # MXFP8 (R13)
+    (2, 2, 8, "bf16", "mxfp8", True),
 ])
 def test_toy_parity_odd(rt, fsdp, tpt, tpg, sdt, ddt, inner):
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, inner)
@@ -113,7 +115,8 @@ def _inject_specials(ol, src):
         b[z:z + 65536] = 0
 
 
-@pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16")])
+@pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16"),
+                                     ("f32", "mxfp8"), ("bf16", "mxfp8")])
 def test_toy_parity_special_values(rt, sdt, ddt):
     # tp_train = 1: no replicated trainer pieces, so injected values stay consistent
     job = _toy_job(rt, "toy", 3, 1, 4, sdt, ddt)
@@ -168,6 +171,16 @@ def _sampled_check(job, n_samples=20000, n_blocks=6, seed=0):
             got = got.view(np.uint32 if es == 4 else np.uint16).astype(np.int64)
             want = harness.expected_elements(ol, 0, g, gp, lr, lc)
             assert np.array_equal(got, want), (g, gp)
+        if cfg.dst_dtype == "mxfp8":
+            qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
+            for gp in rng.choice(qparams, n_blocks, replace=False):
+                R, C, q, off, soff = ol.dst_param(g, int(gp))
+                nsc = -(-C // 32)
+                for r, j in [(0, 0), (R - 1, nsc - 1), (int(rng.integers(R)), int(rng.integers(nsc)))]:
+                    qw, sw = harness.expected_mx_group(ol, 0, g, int(gp), r, j)
+                    codes = t[off + r * C + j * 32:off + r * C + j * 32 + qw.size].cpu().numpy()
+                    assert np.array_equal(codes, qw), (g, gp, r, j)
+                    assert int(t[soff + r * nsc + j].item()) == sw, (g, gp, r, j)
         if cfg.dst_dtype == "fp8":
             qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
             for gp in rng.choice(qparams, n_blocks, replace=False):
@@ -202,6 +215,15 @@ def test_full_c2_8b_sampled(rt):
 def test_full_c4_70b_fp8_sampled(rt):
     """C4 (70B bf16 TP=8 -> fp8 TP=8) at G=1: the 40-layer slice bench.py uses."""
     job = _full_job(rt, "c4")
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=4000, n_blocks=4)
+    job.close()
+
+
+def test_full_c7_70b_mxfp8_sampled(rt):
+    """C7 (70B bf16 TP=8 -> MXFP8 TP=8, NEXT f2) at G=1, 40-layer slice."""
+    job = _full_job(rt, "c7")
     job.sync()
     torch.cuda.synchronize()
     _sampled_check(job, n_samples=4000, n_blocks=4)

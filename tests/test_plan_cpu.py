@@ -39,7 +39,8 @@ def test_library_exports_every_declared_symbol(L):
 
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
     (f, tt, tg, "f32", "bf16", False) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)
-] + [(2, 2, 8, "bf16", "fp8", True), (3, 1, 4, "f32", "fp8", False), (3, 2, 4, "f32", "f32", False)])
+] + [(2, 2, 8, "bf16", "fp8", True), (3, 1, 4, "f32", "fp8", False), (3, 2, 4, "f32", "f32", False),
+      (3, 1, 4, "f32", "mxfp8", False), (2, 2, 8, "bf16", "mxfp8", True)])
 def test_layout_matches_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]
     S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, inner)
@@ -122,7 +123,7 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
                 continue
             x = d["codes"][v.byte_off:v.byte_off + v.rows * v.cols].reshape(v.rows, v.cols)
             assert not np.isnan(x).any()
-            q, s = brute.fp8_quant(x)
+            q, s = brute.mx_quant(x) if dst_dtype == "mxfp8" else brute.fp8_quant(x)
             dst[g][v.byte_off:v.byte_off + q.size] = q.reshape(-1)
             dst[g][v.scale_off:v.scale_off + s.nbytes] = s.view(np.uint8).reshape(-1)
     return dst
@@ -136,6 +137,9 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
     (8, 1, 8, "bf16", "bf16", False, 8),
     (2, 4, 8, "bf16", "bf16", False, 8),
     (1, 8, 8, "bf16", "fp8", False, 8),
+    (3, 1, 4, "f32", "mxfp8", False, 2),
+    (2, 2, 8, "bf16", "mxfp8", True, 4),
+    (8, 1, 8, "bf16", "mxfp8", False, 8),
 ])
 def test_plan_runs_reproduce_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner, G):
     m = MODELS["toy"]
