@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_
 
 constexpr int kCastStageBytes = 32 * 1024;
 constexpr int kCastStages = 4;
-constexpr int kCastWorkers = 128;
+constexpr int kCastWorkers = 384;
 
 // Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
 // item, at most kCastStageBytes of source.  Same enumeration on both roles.
@@ -507,7 +507,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cast_workers_sync() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+__device__ __forceinline__ void cast_workers_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kCastWorkers) : "memory"); }
 
 template <bool SRC_F32>
 __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {

@@ -274,7 +274,7 @@ struct Builder {
         // fp8 blocks: group quantised tiles by (dst rank, dst param)
         std::map<std::pair<int, int>, std::vector<size_t>> by_param;
         for (size_t i = 0; i < P->tiles.size(); i++)
-            if (P->tiles[i].quant) by_param[{P->tiles[i].dst_rank, P->tiles[i].dst_param}].push_back(i);
+            if (P->tiles[i].quant && !mx) by_param[{P->tiles[i].dst_rank, P->tiles[i].dst_param}].push_back(i);
         for (auto &kv : by_param) {
             const int g = kv.first.first;
             const Piece &pc = D->pieces[g][kv.first.second];
