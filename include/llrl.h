@@ -98,12 +98,16 @@ typedef struct {
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
                                  llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
                                  llrl_layout **src_out, llrl_layout **dst_out);
-/* Same, with generator data parallelism (decoupled DP; reading R12):
- * dp_gen replicas of the tp_gen-way generator, generator rank q = d*tp_gen + g
- * holding exactly what TP rank g holds.  llrl_layout_describe == this with
- * dp_gen = 1. */
+/* Same, with generator data parallelism and pipeline stages on either side
+ * (decoupled DP / PP; readings R12, R14): pp_* stages split the
+ * decoder layers evenly and contiguously (embed on the first stage,
+ * final_norm + lm_head on the last; n_layers % pp != 0 -> INDIVISIBLE);
+ * trainer rank = stage*(fsdp*tp_train) + mesh rank, generator rank
+ * q = d*(pp_gen*tp_gen) + stage*tp_gen + g, replica d holding exactly what
+ * replica 0 holds.  Parameters of other stages are empty pieces (0 bytes).
+ * llrl_layout_describe == this with dp_gen = pp_train = pp_gen = 1. */
 typedef struct {
-    int32_t fsdp, tp_train, tp_gen, dp_gen;
+    int32_t fsdp, tp_train, tp_gen, dp_gen, pp_train, pp_gen;
     int32_t src_dtype, dst_dtype;   /* llrl_dtype */
     uint32_t flags;
     int32_t reserved;

@@ -38,7 +38,8 @@ class Model(ctypes.Structure):
 
 class Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("fsdp", "tp_train", "tp_gen", "src_dtype", "dst_dtype", "fsdp_inner", "dp_gen")]
+                ("fsdp", "tp_train", "tp_gen", "src_dtype", "dst_dtype", "fsdp_inner", "dp_gen", "pp_train",
+                 "pp_gen")]
 
 
 _lib = None
@@ -115,12 +116,13 @@ class Layout:
     """The oracle's own view of both layouts for one configuration."""
 
     def __init__(self, model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False,
-                 dp_gen=1):
+                 dp_gen=1, pp_train=1, pp_gen=1):
         m = model
         self.m = Model(m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.head_dim, m.d_ffn, m.vocab, m.with_embed)
-        self.c = Cfg(fsdp, tp_train, tp_gen, DTYPES[src_dtype], DTYPES[dst_dtype], int(fsdp_inner), dp_gen)
+        self.c = Cfg(fsdp, tp_train, tp_gen, DTYPES[src_dtype], DTYPES[dst_dtype], int(fsdp_inner), dp_gen,
+                     pp_train, pp_gen)
         self.src_dtype, self.dst_dtype = src_dtype, dst_dtype
-        self.n_src, self.n_dst = fsdp * tp_train, tp_gen * dp_gen
+        self.n_src, self.n_dst = fsdp * tp_train * pp_train, tp_gen * pp_gen * dp_gen
         L = lib()
         self.status = L.orc_check(ctypes.byref(self.m), ctypes.byref(self.c))
         self.n_src_params = L.orc_num_src_params(ctypes.byref(self.m))

@@ -53,8 +53,11 @@ typedef struct {
 
 typedef struct {
     int32_t fsdp, tp_train, tp_gen, src_dtype, dst_dtype, fsdp_inner;
-    int32_t dp_gen;   /* generator data-parallel replicas (R12); rank q = d*tp_gen + g */
+    int32_t dp_gen;             /* generator data-parallel replicas (R12) */
+    int32_t pp_train, pp_gen;   /* pipeline stages on each side (R14) */
 } orc_cfg;
+/* Rank numbering (R3, R12, R14): trainer rank = stage*(fsdp*tp_train) + mesh
+ * rank; generator rank q = d*(pp_gen*tp_gen) + stage*tp_gen + g. */
 
 /* ------------------------------------------------------------------------ */
 /* Scalar casts                                                              */
@@ -256,6 +259,21 @@ static int layer_slot_to_src_param(const orc_model *m, int layer, int slot)
     return base + 9 * layer + slot;
 }
 
+/* R14: decoder layers split evenly and contiguously over pp stages; embed
+ * lives on the first stage, final_norm and lm_head on the last. */
+static int layer_stage(const orc_model *m, int layer, int first_or_last, int pp)
+{
+    if (layer >= 0)
+        return layer / (m->n_layers / pp);
+    return first_or_last ? pp - 1 : 0;
+}
+
+static int src_param_stage(const orc_model *m, int p, int pp)
+{
+    int layer, slot = src_param_slot(m, p, &layer);
+    return layer_stage(m, layer, slot != SLOT_EMBED, pp);
+}
+
 int orc_src_param_info(const orc_model *m, int p, int64_t *rows, int64_t *cols, int *kind)
 {
     int layer, slot = src_param_slot(m, p, &layer);
@@ -277,8 +295,12 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (m->n_layers < 0 || m->d_model <= 0 || m->n_heads <= 0 || m->n_kv_heads <= 0 ||
         m->head_dim <= 0 || m->d_ffn <= 0 || (m->with_embed && m->vocab <= 0))
         return ORC_E_INVALID;
-    if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0 || c->dp_gen <= 0)
+    if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0 || c->dp_gen <= 0 ||
+        c->pp_train <= 0 || c->pp_gen <= 0)
         return ORC_E_INVALID;
+    /* R14: whole layers per stage */
+    if (m->n_layers % c->pp_train || m->n_layers % c->pp_gen)
+        return ORC_E_INDIVISIBLE;
     if (c->src_dtype != ORC_F32 && c->src_dtype != ORC_BF16)
         return ORC_E_UNSUPPORTED;
     if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_MXFP8)
@@ -311,11 +333,17 @@ static void src_rect(const orc_model *m, const orc_cfg *c, int rank, int p,
                      int64_t *r0, int64_t *r1, int64_t *c0, int64_t *c1)
 {
     int F = c->fsdp, Tt = c->tp_train;
+    int stage = rank / (F * Tt);
+    rank %= F * Tt;
     int f, t;
     if (c->fsdp_inner) { t = rank / F; f = rank % F; }   /* rank = t*F + f */
     else               { f = rank / Tt; t = rank % Tt; } /* rank = f*Tt + t (default) */
     int64_t R, C; int kind;
     orc_src_param_info(m, p, &R, &C, &kind);
+    if (src_param_stage(m, p, c->pp_train) != stage) {   /* R14: not on this stage */
+        *r0 = *r1 = *c0 = *c1 = 0;
+        return;
+    }
     /* TP-local shard */
     int64_t tr0 = 0, tr1 = R, tc0 = 0, tc1 = C;
     if (kind == KIND_COL) { tr0 = t * (R / Tt); tr1 = tr0 + R / Tt; }
@@ -391,7 +419,7 @@ static int dst_param_slot(const orc_model *m, int gp, int *layer)
 typedef struct { int src_param; int64_t fr0, fc0, nr, nc, lr0; } part_t;
 
 /* Local shape of generator param gp on rank g and its parts (<= 3). */
-static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int gp,
+static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int stage, int gp,
                      int64_t *rows, int64_t *cols, int *quant, part_t *parts)
 {
     int T = c->tp_gen, layer, gs = dst_param_slot(m, gp, &layer);
@@ -454,6 +482,10 @@ static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int gp,
     }
     if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8)
         *quant = 0;
+    if (stage >= 0 && layer_stage(m, layer, gs != G_EMBED, c->pp_gen) != stage) {
+        *rows = 0; *cols = 0;          /* R14: not on this generator stage */
+        return 0;
+    }
     return n;
 }
 
@@ -475,12 +507,14 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
                   int64_t *rows, int64_t *cols, int *quant,
                   int64_t *byte_off, int64_t *scale_off)
 {
-    g %= c->tp_gen;   /* R12: replica d's rank d*T + g holds what TP rank g holds */
+    /* R12 / R14: generator rank -> (TP rank, pipeline stage); replicas repeat */
+    int stage = (g / c->tp_gen) % c->pp_gen;
+    g %= c->tp_gen;
     int64_t off = 0;
     for (int q = 0; q <= gp; q++) {
         part_t parts[3];
         int64_t R, C; int qt;
-        if (dst_parts(m, c, g, q, &R, &C, &qt, parts) < 0)
+        if (dst_parts(m, c, g, stage, q, &R, &C, &qt, parts) < 0)
             return ORC_E_INVALID;
         int64_t es = qt ? 1 : (c->dst_dtype == ORC_F32 ? 4 : 2);
         off = align256(off);
@@ -502,7 +536,6 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
 
 int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
 {
-    g %= c->tp_gen;
     int P = orc_num_dst_params(m);
     if (P == 0)
         return 0;
@@ -520,10 +553,11 @@ int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
 int orc_dst_element_source(const orc_model *m, const orc_cfg *c, int g, int gp,
                            int64_t lr, int64_t lc, int *src_param, int64_t *row, int64_t *col)
 {
+    int stage = (g / c->tp_gen) % c->pp_gen;
     g %= c->tp_gen;
     part_t parts[3];
     int64_t R, C; int qt;
-    int n = dst_parts(m, c, g, gp, &R, &C, &qt, parts);
+    int n = dst_parts(m, c, g, stage, gp, &R, &C, &qt, parts);
     if (n < 0 || lr < 0 || lr >= R || lc < 0 || lc >= C)
         return ORC_E_INVALID;
     for (int i = 0; i < n; i++)
@@ -563,7 +597,7 @@ static int materialise(const orc_model *m, const orc_cfg *c, const void *const *
     float *full = (float *)malloc((size_t)(R * C > 0 ? R * C : 1) * sizeof(float));
     uint8_t *seen = (uint8_t *)calloc((size_t)(R * C > 0 ? R * C : 1), 1);
     if (!full || !seen) { free(full); free(seen); return ORC_E_NOMEM; }
-    int nsrc = c->fsdp * c->tp_train;
+    int nsrc = c->fsdp * c->tp_train * c->pp_train;
     for (int s = 0; s < nsrc; s++) {
         int64_t r0, r1, c0, c1;
         int64_t off = orc_src_piece(m, c, s, p, &r0, &r1, &c0, &c1);
@@ -607,7 +641,7 @@ static int write_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
 {
     part_t parts[3];
     int64_t R, C, off, soff; int qt;
-    int n = dst_parts(m, c, g, gp, &R, &C, &qt, parts);
+    int n = dst_parts(m, c, g % c->tp_gen, (g / c->tp_gen) % c->pp_gen, gp, &R, &C, &qt, parts);
     orc_dst_param(m, c, g, gp, &R, &C, &qt, &off, &soff);
     /* Step 2: the generator-local (fused) tensor */
     float *local = (float *)malloc((size_t)(R * C > 0 ? R * C : 1) * sizeof(float));
@@ -677,7 +711,7 @@ int orc_sync_range(const orc_model *m, const orc_cfg *c, const void *const *src,
     int rc = check_model(m, c);
     if (rc)
         return rc;
-    int P = orc_num_src_params(m), T = c->tp_gen, ND = c->tp_gen * c->dp_gen;
+    int P = orc_num_src_params(m), ND = c->tp_gen * c->pp_gen * c->dp_gen;
     float **full = (float **)calloc((size_t)(P > 0 ? P : 1), sizeof(float *));
     uint8_t **written = (uint8_t **)calloc((size_t)ND, sizeof(uint8_t *));
     if (!full || !written) { free(full); free(written); return ORC_E_NOMEM; }
@@ -688,12 +722,12 @@ int orc_sync_range(const orc_model *m, const orc_cfg *c, const void *const *src,
     for (int gp = gp_begin; gp < gp_end && rc == ORC_OK; gp++) {
         part_t parts[3];
         int64_t R, C; int qt;
-        int n = dst_parts(m, c, 0, gp, &R, &C, &qt, parts);
+        int n = dst_parts(m, c, 0, -1, gp, &R, &C, &qt, parts);
         for (int i = 0; i < n && rc == ORC_OK; i++)
             if (!full[parts[i].src_param])
                 rc = materialise(m, c, src, parts[i].src_param, &full[parts[i].src_param]);
-        for (int q = 0; q < ND && rc == ORC_OK; q++)   /* every replica gets its own copy */
-            rc = write_dst_param(m, c, q % T, gp, full, (uint8_t *)dst[q], written[q]);
+        for (int q = 0; q < ND && rc == ORC_OK; q++)   /* every stage rank / replica writes its own copy */
+            rc = write_dst_param(m, c, q, gp, full, (uint8_t *)dst[q], written[q]);
         for (int i = 0; i < n; i++) {
             free(full[parts[i].src_param]);
             full[parts[i].src_param] = NULL;

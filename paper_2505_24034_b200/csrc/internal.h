@@ -75,7 +75,7 @@ struct DstParamDesc {
 struct llrl_layout {
     bool is_src;
     llrl_model model;
-    int fsdp, tp_train, tp_gen, dp_gen;
+    int fsdp, tp_train, tp_gen, dp_gen, pp_train, pp_gen;
     int dtype;          // src: data dtype; dst: target dtype (F32/BF16/FP8)
     uint32_t flags;
     int n_ranks;

@@ -72,6 +72,12 @@ void mesh_coords(int rank, int fsdp, int tp, uint32_t flags, int *f, int *t) {
     else { *f = rank / tp; *t = rank % tp; }
 }
 
+// R14: pipeline stage of a layer (-1: embed -> first stage; -2: head -> last).
+int stage_of(const llrl_model &m, int kind, int layer, int pp) {
+    if (layer >= 0) return layer / (m.n_layers / pp);
+    return kind == LLRL_P_EMBED ? 0 : pp - 1;
+}
+
 // R1 then R2: Megatron TP rectangle, then torch.chunk of its rows over FSDP.
 Rect trainer_rect(const SrcParam &p, int f, int t, int fsdp, int tp) {
     Rect r{0, p.rows, 0, p.cols};
@@ -96,18 +102,23 @@ llrl_status build_src(llrl_layout *L) {
         if (p.split == 0 && p.rows % L->tp_train) return LLRL_E_INDIVISIBLE;
         if (p.split == 1 && p.cols % L->tp_train) return LLRL_E_INDIVISIBLE;
     }
-    L->n_ranks = L->fsdp * L->tp_train;
+    if (L->model.n_layers % L->pp_train) return LLRL_E_INDIVISIBLE;
+    const int mesh = L->fsdp * L->tp_train;
+    L->n_ranks = mesh * L->pp_train;
     const int64_t es = dtype_bytes(L->dtype);
     L->pieces.assign(L->n_ranks, {});
     L->rank_bytes.assign(L->n_ranks, 0);
     for (int r = 0; r < L->n_ranks; r++) {
         int f, t;
-        mesh_coords(r, L->fsdp, L->tp_train, L->flags, &f, &t);
+        const int stage = r / mesh;
+        mesh_coords(r % mesh, L->fsdp, L->tp_train, L->flags, &f, &t);
         int64_t off = 0;
         for (size_t i = 0; i < ps.size(); i++) {
             Piece pc;
             pc.param = int(i);
-            pc.rect = trainer_rect(ps[i], f, t, L->fsdp, L->tp_train);
+            pc.rect = stage_of(L->model, ps[i].kind, ps[i].layer, L->pp_train) == stage
+                          ? trainer_rect(ps[i], f, t, L->fsdp, L->tp_train)
+                          : Rect{};
             pc.rows = pc.rect.rows();
             pc.cols = pc.rect.cols();
             off = align_up(off);
@@ -129,6 +140,7 @@ llrl_status build_dst(llrl_layout *L) {
     if (m.n_kv_heads % T && T % m.n_kv_heads) return LLRL_E_INDIVISIBLE;
     if (m.d_ffn % T) return LLRL_E_INDIVISIBLE;
     if (m.with_embed && m.vocab % T) return LLRL_E_INDIVISIBLE;
+    if (m.n_layers % L->pp_gen) return LLRL_E_INDIVISIBLE;
     const auto &ps = L->src_params;
     auto &dp = L->dst_params;
     dp.clear();
@@ -152,10 +164,12 @@ llrl_status build_dst(llrl_layout *L) {
     const int64_t f_local = m.d_ffn / T;
     const int64_t v_local = m.with_embed ? m.vocab / T : 0;
 
-    L->n_ranks = T;
-    L->pieces.assign(T, {});
-    L->rank_bytes.assign(T, 0);
-    for (int g = 0; g < T; g++) {
+    const int NS = T * L->pp_gen;           // ranks of one replica: stage*T + g
+    L->n_ranks = NS;
+    L->pieces.assign(size_t(NS), {});
+    L->rank_bytes.assign(size_t(NS), 0);
+    for (int sg = 0; sg < NS; sg++) {
+        const int stage = sg / T, g = sg % T;
         const int64_t kv_row0 = kv_split ? g * kv_local : int64_t(g / (T / m.n_kv_heads)) * hd;
         int64_t off = 0;
         for (size_t i = 0; i < dp.size(); i++) {
@@ -194,6 +208,11 @@ llrl_status build_dst(llrl_layout *L) {
             default:
                 return LLRL_E_INVALID;
             }
+            if (stage_of(m, dp[i].kind, l, L->pp_gen) != stage) {   // R14: another stage's tensor
+                pc.rows = 0;
+                pc.cols = 0;
+                pc.parts.clear();
+            }
             pc.rect = Rect{0, pc.rows, 0, pc.cols};
             pc.quantised = (L->dtype == LLRL_FP8_E4M3 || L->dtype == LLRL_MXFP8) && dp[i].quantisable;
             pc.dtype = pc.quantised ? L->dtype : (L->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
@@ -205,17 +224,17 @@ llrl_status build_dst(llrl_layout *L) {
                 pc.scale_off = off;
                 off += scale_grid_bytes(L->dtype, pc.rows, pc.cols);
             }
-            L->pieces[g].push_back(pc);
+            L->pieces[size_t(sg)].push_back(pc);
         }
-        L->rank_bytes[g] = align_up(off);
+        L->rank_bytes[size_t(sg)] = align_up(off);
     }
-    // R12: generator DP replicas -- rank d*T + g is laid out exactly like TP rank g
+    // R12: generator DP replicas -- rank d*NS + q is laid out exactly like rank q
     for (int d = 1; d < L->dp_gen; d++)
-        for (int g = 0; g < T; g++) {
-            L->pieces.push_back(L->pieces[size_t(g)]);
-            L->rank_bytes.push_back(L->rank_bytes[size_t(g)]);
+        for (int q = 0; q < NS; q++) {
+            L->pieces.push_back(L->pieces[size_t(q)]);
+            L->rank_bytes.push_back(L->rank_bytes[size_t(q)]);
         }
-    L->n_ranks = T * L->dp_gen;
+    L->n_ranks = NS * L->dp_gen;
     return LLRL_OK;
 }
 
@@ -234,11 +253,11 @@ const char *llrl_version(void) { return "llrl 0.1 (sm_100a)"; }
 llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts *o, llrl_layout **src_out,
                                     llrl_layout **dst_out) {
     if (!o || !src_out || !dst_out || !model_ok(m) || o->fsdp <= 0 || o->tp_train <= 0 || o->tp_gen <= 0 ||
-        o->dp_gen <= 0) {
+        o->dp_gen <= 0 || o->pp_train <= 0 || o->pp_gen <= 0) {
         set_error("llrl_layout_describe: invalid argument");
         return LLRL_E_INVALID;
     }
-    if (o->fsdp * o->tp_train > kMaxRanks || o->tp_gen * o->dp_gen > kMaxRanks) {
+    if (o->fsdp * o->tp_train * o->pp_train > kMaxRanks || o->tp_gen * o->dp_gen * o->pp_gen > kMaxRanks) {
         set_error("llrl_layout_describe: at most %d ranks per side", kMaxRanks);
         return LLRL_E_INVALID;
     }
@@ -255,6 +274,7 @@ llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts 
     for (llrl_layout *L : {S, D}) {
         L->model = *m;
         L->fsdp = o->fsdp; L->tp_train = o->tp_train; L->tp_gen = o->tp_gen; L->dp_gen = o->dp_gen;
+        L->pp_train = o->pp_train; L->pp_gen = o->pp_gen;
         L->flags = o->flags;
         L->src_params = enumerate_src_params(*m);
     }
@@ -275,7 +295,7 @@ llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts 
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
                                  llrl_dtype src_dtype, llrl_dtype dst_dtype, uint32_t flags,
                                  llrl_layout **src_out, llrl_layout **dst_out) {
-    const llrl_layout_opts o{fsdp, tp_train, tp_gen, 1, src_dtype, dst_dtype, flags, 0};
+    const llrl_layout_opts o{fsdp, tp_train, tp_gen, 1, 1, 1, src_dtype, dst_dtype, flags, 0};
     return llrl_layout_describe_ex(m, &o, src_out, dst_out);
 }
 

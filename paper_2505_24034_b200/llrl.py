@@ -50,8 +50,9 @@ class ModelDesc(ctypes.Structure):
 
 class LayoutOpts(ctypes.Structure):
     _fields_ = [("fsdp", ctypes.c_int32), ("tp_train", ctypes.c_int32), ("tp_gen", ctypes.c_int32),
-                ("dp_gen", ctypes.c_int32), ("src_dtype", ctypes.c_int32), ("dst_dtype", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
+                ("dp_gen", ctypes.c_int32), ("pp_train", ctypes.c_int32), ("pp_gen", ctypes.c_int32),
+                ("src_dtype", ctypes.c_int32), ("dst_dtype", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("reserved", ctypes.c_int32)]
 
 
 class ParamView(ctypes.Structure):
@@ -171,11 +172,12 @@ class Layout:
     __del__ = close
 
 
-def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False, dp_gen=1):
+def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False, dp_gen=1,
+             pp_train=1, pp_gen=1):
     """llrl_layout_describe_ex -> (src Layout, dst Layout)."""
     m = ModelDesc(model.n_layers, model.d_model, model.n_heads, model.n_kv_heads, model.head_dim, model.d_ffn,
                   model.vocab, model.with_embed)
-    o = LayoutOpts(fsdp, tp_train, tp_gen, dp_gen, DTYPES[src_dtype], DTYPES[dst_dtype],
+    o = LayoutOpts(fsdp, tp_train, tp_gen, dp_gen, pp_train, pp_gen, DTYPES[src_dtype], DTYPES[dst_dtype],
                    MESH_FSDP_INNER if fsdp_inner else 0, 0)
     s, d = _vp(), _vp()
     _check(_lib.llrl_layout_describe_ex(ctypes.byref(m), ctypes.byref(o), ctypes.byref(s), ctypes.byref(d)))

@@ -59,7 +59,7 @@ class SyncJob:
         self.device = self.rank if device is None else device
         torch.cuda.set_device(self.device)
         self.S, self.D = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype,
-                                       cfg.dst_dtype, cfg.fsdp_inner, cfg.dp_gen)
+                                       cfg.dst_dtype, cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
         self.src_dev, self.dst_dev = placement(cfg, spec.n_gpus)
         self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev)
         dev = torch.device("cuda", self.device)

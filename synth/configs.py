@@ -49,14 +49,16 @@ class LayoutConfig:
     fsdp_inner: bool = False
     notes: str = ""
     dp_gen: int = 1         # generator data-parallel replicas (R12)
+    pp_train: int = 1       # pipeline stages (R14)
+    pp_gen: int = 1
 
     @property
     def n_src(self) -> int:
-        return self.fsdp * self.tp_train
+        return self.fsdp * self.tp_train * self.pp_train
 
     @property
     def n_dst(self) -> int:
-        return self.tp_gen * self.dp_gen
+        return self.tp_gen * self.pp_gen * self.dp_gen
 
 
 CONFIGS = {
@@ -77,6 +79,10 @@ CONFIGS = {
     # NEXT f2: MX formats for the generator, as tcgen05 block-scaled MMA consumes them
     "c7": LayoutConfig("c7", "llama3-70b", 1, 8, 8, "bf16", "mxfp8", "colocated",
                        notes="70B bf16 TP=8 -> MXFP8 TP=8 (E4M3 + E8M0 per 1x32)"),
+    # NEXT f4: decoupled pipeline parallelism -- a PP=2 trainer
+    # (FSDP=2 x TP=2 per stage) re-staged into a PP-less TP=8 generator.
+    "c8": LayoutConfig("c8", "llama3-70b", 2, 2, 8, "bf16", "bf16", "colocated", pp_train=2,
+                       notes="70B bf16 PP=2 x FSDP=2 x TP=2 -> bf16 TP=8 (layer re-staging)"),
 }
 
 

@@ -26,10 +26,10 @@ from synth import LayoutConfig  # noqa: E402
 from tests import harness  # noqa: E402
 
 
-def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2, dp=1):
-    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner, dp_gen=dp)
+def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2, dp=1, ppt=1, ppg=1):
+    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner, dp_gen=dp, pp_train=ppt, pp_gen=ppg)
     job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False)
-    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner, dp)
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner, dp, ppt, ppg)
     for rep in range(reps):
         src = harness.host_src(ol, seed + rep)
         for r, t in job.src.items():
@@ -116,6 +116,8 @@ def main():
             print("ok", c, flush=True)
     toy_case(runner, world, 4, 1, 1, "f32", "bf16", "disjoint", dp=4)      # generator DP replicas
     toy_case(runner, world, 2, 2, 2, "bf16", "fp8", "disjoint", dp=2)
+    toy_case(runner, world, 2, 2, 8, "bf16", "bf16", "colocated", ppt=2)       # pipeline re-staging
+    toy_case(runner, world, 3, 1, 2, "f32", "mxfp8", "disjoint", ppt=2, ppg=2, dp=2)
     if "--full" in sys.argv:
         for name in ("c2", "c3"):
             full_case(runner, world, name)

@@ -28,16 +28,17 @@ def rt():
     return llrl, runner
 
 
-def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None, dp=1):
+def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None, dp=1, ppt=1, ppg=1):
     llrl, runner = rt
-    cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner, dp_gen=dp)
+    cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner, dp_gen=dp, pp_train=ppt,
+                       pp_gen=ppg)
     return runner.SyncJob(runner.JobSpec(cfg, 1, n_layers=n_layers), fill=False)
 
 
 def _run_and_compare(rt, job, seed, sentinel=0xA5, inject=None):
     cfg = job.cfg
     ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
-                       cfg.dp_gen)
+                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
     src = harness.host_src(ol, seed)
     if inject is not None:
         inject(ol, src)
@@ -132,6 +133,15 @@ def test_toy_parity_generator_dp(rt, fsdp, tpt, tpg, dp, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("fsdp,tpt,ppt,tpg,ppg,dp,sdt,ddt", [
+    (2, 1, 2, 2, 1, 1, "f32", "bf16"), (1, 2, 1, 2, 2, 1, "bf16", "fp8"), (3, 1, 2, 4, 2, 2, "f32", "mxfp8")])
+def test_toy_parity_pipeline_stages(rt, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
+    """Decoupled pipeline parallelism (R14), with and without DP replicas."""
+    job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, dp=dp, ppt=ppt, ppg=ppg)
+    _run_and_compare(rt, job, seed=17)
+    job.close()
+
+
 def test_toy_parity_repeated_syncs(rt):
     """The same plan run many times (epoch counters, no stale state)."""
     job = _toy_job(rt, "toy", 4, 1, 4, "f32", "bf16")
@@ -152,7 +162,8 @@ def _full_job(rt, name, n_layers=None):
 
 def _sampled_check(job, n_samples=20000, n_blocks=6, seed=0):
     cfg = job.cfg
-    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
+    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
     rng = np.random.default_rng(1)
     for g, t in job.dst.items():
         n_params = ol.n_dst_params

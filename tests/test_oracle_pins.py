@@ -217,6 +217,25 @@ def test_oracle_vs_brute_generator_dp(oracle_lib, fsdp, tpt, tpg, dp, sdt, ddt):
         assert np.array_equal(d, w)
 
 
+@pytest.mark.parametrize("fsdp,tpt,ppt,tpg,ppg,dp,sdt,ddt", [
+    (2, 1, 2, 2, 1, 1, "f32", "bf16"),     # trainer PP=2 -> generator without PP
+    (1, 2, 1, 2, 2, 1, "bf16", "fp8"),     # generator PP=2
+    (3, 1, 2, 4, 2, 2, "f32", "mxfp8"),    # both sides staged, with DP replicas
+])
+def test_oracle_vs_brute_pipeline_stages(oracle_lib, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
+    """Decoupled pipeline parallelism (R14): layer -> stage maps differ per side."""
+    m = MODELS["toy"]
+    src, want = brute.build(m, 21, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp, pp_train=ppt, pp_gen=ppg)
+    L = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, False, dp, ppt, ppg)
+    assert L.status == 0 and L.n_src == len(src) and L.n_dst == len(want)
+    assert [L.src_rank_bytes(r) for r in range(L.n_src)] == [b.size for b in src]
+    dst = [np.zeros(L.dst_rank_bytes(q), np.uint8) for q in range(L.n_dst)]
+    assert L.sync(src, dst) == 0
+    for d, w in zip(dst, want):
+        assert np.array_equal(d, w)
+    assert oracle.Layout(m, 1, 1, 1, sdt, ddt, False, 1, 3, 1).status == oracle.E_INDIVISIBLE   # 2 layers / 3
+
+
 def test_oracle_provenance_closed_form(oracle_lib):
     """f32 -> f32 identity: every generator element equals the generator value of
     the source coordinate given in closed form by readings R4 (no brute force)."""

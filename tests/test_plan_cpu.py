@@ -79,6 +79,34 @@ def test_generator_dp_layout_and_plan(L, fsdp, tpt, tpg, dp, sdt, ddt, G):
         assert np.array_equal(got[q], want[q]), q
 
 
+@pytest.mark.parametrize("fsdp,tpt,ppt,tpg,ppg,dp,sdt,ddt,G", [
+    (2, 1, 2, 2, 1, 1, "f32", "bf16", 4), (1, 2, 1, 2, 2, 1, "bf16", "fp8", 4),
+    (3, 1, 2, 4, 2, 2, "f32", "mxfp8", 8), (2, 2, 2, 8, 1, 1, "bf16", "bf16", 8)])
+def test_pipeline_stages_layout_and_plan(L, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt, G):
+    """Decoupled PP (R14): product layouts == oracle's; plan runs == oracle bytes."""
+    m = MODELS["toy"]
+    S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp, pp_train=ppt, pp_gen=ppg)
+    O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, False, dp, ppt, ppg)
+    assert S.n_ranks == O.n_src and D.n_ranks == O.n_dst
+    for r in range(S.n_ranks):
+        assert S.rank_bytes(r) == O.src_rank_bytes(r)
+        for p in range(S.n_params):
+            v = S.param_view(r, p)
+            off, r0, r1, c0, c1 = O.src_piece(r, p)
+            assert v.byte_off == off and v.rows == r1 - r0 and v.cols == c1 - c0
+    for q in range(D.n_ranks):
+        assert D.rank_bytes(q) == O.dst_rank_bytes(q)
+        for gp in range(D.n_params):
+            v = D.param_view(q, gp)
+            assert (v.rows, v.cols, v.quantised, v.byte_off, v.scale_off) == O.dst_param(q, gp)
+    ns, nd = S.n_ranks, D.n_ranks
+    plan = L.Plan(S, D, [r * G // ns for r in range(ns)], [q * G // nd for q in range(nd)])
+    src, want = brute.build(m, 9, fsdp, tpt, tpg, sdt, ddt, dp_gen=dp, pp_train=ppt, pp_gen=ppg)
+    got = _interpret(L, plan, D, src, sdt, ddt, [w.size for w in want])
+    for q in range(nd):
+        assert np.array_equal(got[q], want[q]), q
+
+
 def test_layout_errors(L):
     m = MODELS["toy"]
     for args, st in [((1, 1, 3), L.E_INDIVISIBLE), ((1, 1, 16), L.E_INDIVISIBLE), ((1, 3, 2), L.E_INDIVISIBLE),
@@ -86,6 +114,9 @@ def test_layout_errors(L):
         with pytest.raises(L.LlrlError) as e:
             L.describe(m, *args)
         assert e.value.status == st
+    with pytest.raises(L.LlrlError) as e:
+        L.describe(m, 1, 1, 2, pp_train=3)        # 2 layers over 3 stages
+    assert e.value.status == L.E_INDIVISIBLE
     with pytest.raises(L.LlrlError) as e:
         L.describe(m, 1, 1, 2, "bf16", "f32")
     assert e.value.status == L.E_UNSUPPORTED
