@@ -455,9 +455,7 @@ struct Builder {
                 const DstParamDesc &dpd = D->dst_params[size_t(pc.param)];
                 auto &rg = P->dst_group_range[size_t(g)][size_t(group_of(dpd.kind, dpd.layer))];
                 widen(rg, pc.byte_off, pc.byte_off + pc.rows * pc.cols * dtype_bytes(pc.dtype));
-                if (pc.quantised)
-                    widen(rg, pc.scale_off, pc.scale_off + ((pc.rows + kFp8Block - 1) / kFp8Block) *
-                                                               ((pc.cols + kFp8Block - 1) / kFp8Block) * 4);
+                if (pc.quantised) widen(rg, pc.scale_off, pc.scale_off + scale_grid_bytes(pc.dtype, pc.rows, pc.cols));
             }
         return LLRL_OK;
     }
