@@ -219,7 +219,10 @@ def run_llrl(args):
     spec = runner.spec_for(args.config, args.gpus)
     if args.layers is not None:           # profiling only (ncu replay of a smaller model)
         spec = runner.JobSpec(spec.cfg, spec.n_gpus, n_layers=args.layers)
-    job = runner.SyncJob(spec, device=local, seed=0)
+    if args.placement:
+        import dataclasses
+        spec = runner.JobSpec(dataclasses.replace(spec.cfg, placement=args.placement), spec.n_gpus, spec.n_layers)
+    job = runner.SyncJob(spec, device=local, seed=0, multicast=args.multicast)
     cfg = job.cfg
     stream = job.stream
 
@@ -288,6 +291,8 @@ def run_llrl(args):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": "synthetic (counter-based Llama-init-scale weights)",
             "config": {"workload": _workload_name(cfg, args.gpus), "model": cfg.model,
+                       "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
+                       "multicast": bool(args.multicast and job.mc_positions()[0]),
                        "layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
                        "l2": "inputs >> 126 MB L2 (no flush needed)"},
@@ -366,6 +371,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers", type=int, default=None, help="override decoder layers (profiling only)")
+    ap.add_argument("--placement", default=None, choices=["disjoint", "colocated", "rotated"])
+    ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

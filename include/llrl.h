@@ -132,6 +132,10 @@ void llrl_layout_destroy(llrl_layout *l);
 llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst,
                              const int *src_device, const int *dst_device, uint32_t flags,
                              llrl_plan **out);
+/* flags of llrl_plan_create */
+#define LLRL_PLAN_MULTICAST 1u   /* NEXT f1: write generator DP replicas once through NVLS
+                                    multicast (see llrl_mc_*); positions whose replicas share
+                                    a GPU fall back to per-replica pushes */
 void llrl_plan_destroy(llrl_plan *p);
 
 /* A canonical 1-D run: `len` consecutive elements (verification view). */
@@ -188,6 +192,25 @@ llrl_status llrl_comm_export(const llrl_comm *c, void *handle64);
 llrl_status llrl_comm_import(llrl_comm *c, int peer_device, const void *handle64);
 llrl_status llrl_comm_flag_ptr(const llrl_comm *c, void **dev_ptr);
 llrl_status llrl_comm_set_peer(llrl_comm *c, int peer_device, void *peer_flag_dev_ptr);
+/* ---- NVLS multicast buffers (NEXT f1) -----------------------------------------
+ * One multicast object per generator rank position (TP rank x PP stage) whose
+ * replicas live on different GPUs; its team is every GPU of the job.  The
+ * creating process calls llrl_mc_create (size rounded up to the multicast
+ * granularity; *fd_out is a POSIX file descriptor to pass to the other
+ * processes, e.g. over a Unix socket with SCM_RIGHTS), the others
+ * llrl_mc_import; then every process calls llrl_mc_join for its GPU, which
+ * creates and binds that GPU's physical memory and maps it at a unicast VA
+ * (*local_ptr: use it as the generator rank buffer on replica GPUs; scratch
+ * elsewhere) and maps the multicast VA (*mc_ptr).  llrl_plan_set_multicast
+ * gives a device the multicast VA of every generator rank (NULL where none).
+ * Errors: UNSUPPORTED (no multicast driver support), CUDA. */
+typedef struct llrl_mcbuf llrl_mcbuf;
+llrl_status llrl_mc_create(int n_devices, int64_t bytes, int *fd_out, int64_t *size_out, llrl_mcbuf **out);
+llrl_status llrl_mc_import(int fd, int n_devices, int64_t size, llrl_mcbuf **out);
+llrl_status llrl_mc_join(llrl_mcbuf *m, int device, void **local_ptr, void **mc_ptr);
+void llrl_mc_destroy(llrl_mcbuf *m);
+llrl_status llrl_plan_set_multicast(llrl_plan *p, int device, void *const *dst_mc_ptrs);
+
 /* Synchronous check of the timeout flag (1 if any wait on this device gave up). */
 llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out);
 void llrl_comm_destroy(llrl_comm *c);

@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libllrl.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["layout.cpp", "plan.cpp", "runtime.cu", "kernels.cu", "init.cu"]
+SOURCES = ["layout.cpp", "plan.cpp", "runtime.cu", "kernels.cu", "init.cu", "multicast.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 

@@ -103,6 +103,7 @@ enum ItemFlag : uint16_t {
     F_VEC = 1,         // 16-byte vector path legal (offsets / lds / cols aligned)
     F_DST_F32 = 2,     // destination dtype f32 (identity), else bf16 (K_CAST)
     F_MX = 4,          // K_CAST into MXFP8 codes (1 byte); aux = scale byte base (R13)
+    F_MC = 8,          // K_CAST stored through the NVLS multicast VA of dst_rank's position (f1)
 };
 
 // Device work item (48 bytes).  Offsets in elements of each side's dtype, except
@@ -156,6 +157,8 @@ struct DeviceWork {
     std::vector<Item> items;
     std::vector<Seg> segs;
     std::vector<TmaRef> tma_refs;      // one per fp8 item (index i - n_cast)
+    std::vector<void *> dst_mc;        // multicast VA per dst rank (llrl_plan_set_multicast)
+    bool has_mc = false;
     std::vector<TmaPiece> tma_pieces;
     std::vector<int> signal_devices;   // devices this device writes into (excl. itself)
     int n_senders_in = 0;              // other devices writing into this device
@@ -192,6 +195,7 @@ struct DeviceWork {
 
 struct llrl_plan {
     int n_src, n_dst, n_devices;
+    bool multicast = false;
     int src_dtype, dst_dtype;
     std::vector<int> src_device, dst_device;
     std::vector<int64_t> src_rank_bytes, dst_rank_bytes;

@@ -42,6 +42,20 @@ __device__ __forceinline__ void st_v4(void *p, uint4 v) {
                  : "memory");
 }
 
+// NVLS multicast stores (f1): one store, replicated by the NVSwitch to every
+// GPU bound to the multicast object.  Bit patterns pass through unchanged
+// (no arithmetic on a store).
+__device__ __forceinline__ void mc_st_v4(void *p, uint4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+}
+__device__ __forceinline__ void mc_st_v2(void *p, uint32_t x, uint32_t y) {
+    asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(__uint_as_float(x)),
+                 "f"(__uint_as_float(y))
+                 : "memory");
+}
+
 // RNE fp32 -> bf16 of two values; `lo` lands in the low half (lower address).
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
     uint32_t r;
@@ -85,6 +99,8 @@ __device__ __forceinline__ void cast_item(const Item &it, const KParams &P) {
         const int upr = it.cols / E;                 // units per row
         const int nunits = it.rows * upr;
         const bool one_d = it.rows == 1;
+        const bool mc = it.flags & F_MC;
+        if (mc) dst = static_cast<char *>(P.dst_mc[it.dst_rank]);
         const char *sbase = src + it.src_off * es;
         char *dbase = dst + it.dst_off * (dst_f32 ? 4 : 2);
         for (int u0 = threadIdx.x; u0 < nunits; u0 += kThreads * U) {
@@ -106,14 +122,19 @@ __device__ __forceinline__ void cast_item(const Item &it, const KParams &P) {
                 if (!one_d) { r = u / upr; c = (u - r * upr) * E; }
                 const int64_t doff = int64_t(r) * it.dst_ld + c;
                 if (SRC_F32 && !dst_f32) {
-                    st_v2(dbase + doff * 2, bf16x2_rn(__uint_as_float(a[k].x), __uint_as_float(a[k].y)),
-                          bf16x2_rn(__uint_as_float(a[k].z), __uint_as_float(a[k].w)));
+                    const uint32_t lo = bf16x2_rn(__uint_as_float(a[k].x), __uint_as_float(a[k].y));
+                    const uint32_t hi = bf16x2_rn(__uint_as_float(a[k].z), __uint_as_float(a[k].w));
+                    if (mc) mc_st_v2(dbase + doff * 2, lo, hi);
+                    else st_v2(dbase + doff * 2, lo, hi);
+                } else if (mc) {
+                    mc_st_v4(dbase + doff * es, a[k]);
                 } else {
                     st_v4(dbase + doff * es, a[k]);   // identity (f32->f32, bf16->bf16)
                 }
             }
         }
     } else {
+        if (it.flags & F_MC) dst = static_cast<char *>(P.dst_mc[it.dst_rank]);   // plain stores to the MC VA
         const int n = it.rows * it.cols;
         for (int e = threadIdx.x; e < n; e += kThreads) {
             const int r = e / it.cols, c = e - r * it.cols;

@@ -23,6 +23,7 @@ struct KParams {
     unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
     const void *src[kMaxRanks];
     void *dst[kMaxRanks];
+    void *dst_mc[kMaxRanks];           // multicast VA per dst rank (F_MC items)
 };
 
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)

@@ -44,6 +44,19 @@ struct Builder {
     llrl_plan *P;
     int64_t es_src, es_dst;
 
+    // Generator DP replicas (R12): rank q = d*NS + position.  A position is
+    // multicast-eligible when the plan asks for it and its replicas sit on
+    // pairwise different GPUs.
+    int n_pos() const { return D->n_ranks / D->dp_gen; }
+    bool mc_position(int pos) const {
+        if (!P->multicast || D->dp_gen < 2) return false;
+        for (int a = 0; a < D->dp_gen; a++)
+            for (int b = a + 1; b < D->dp_gen; b++)
+                if (P->dst_device[size_t(a * n_pos() + pos)] == P->dst_device[size_t(b * n_pos() + pos)]) return false;
+        return true;
+    }
+    std::vector<std::vector<std::vector<int>>> mc_extra;   // [exec dev][group] -> replica devices to signal
+
     int holder(const std::vector<int> &members, int g) const {
         for (int r : members)
             if (P->src_device[r] == P->dst_device[g]) return r;   // same GPU first (R5)
@@ -256,6 +269,7 @@ struct Builder {
         n_groups = S->model.n_layers + (S->model.with_embed ? 2 : 0);
         P->n_groups = n_groups;
         lists.assign(G, std::vector<std::vector<std::vector<Item>>>(G, std::vector<std::vector<Item>>(n_groups)));
+        mc_extra.assign(size_t(G), std::vector<std::vector<int>>(size_t(n_groups)));
         seglists.assign(G, {});
         // bf16 / f32 tiles, and MXFP8 tiles (row-wise 1x32 groups ride on cast items, R13)
         const bool mx = D->dtype == LLRL_MXFP8;
@@ -268,8 +282,38 @@ struct Builder {
             }
             const int sd = P->src_device[t.src_rank], dd = P->dst_device[t.dst_rank];
             const SrcParam &sp = S->src_params[size_t(t.src_param)];
-            add_cast_items(t, lists[sd][dd][size_t(group_of(sp.kind, sp.layer))]);
-            account(sd, sd, dd, t.rows * t.cols * es_src, t.rows * t.cols * es_dst, false);
+            const size_t grp = size_t(group_of(sp.kind, sp.layer));
+            const int pos = t.dst_rank % n_pos(), rep = t.dst_rank / n_pos();
+            if (!mc_position(pos)) {
+                add_cast_items(t, lists[sd][dd][grp]);
+                account(sd, sd, dd, t.rows * t.cols * es_src, t.rows * t.cols * es_dst, false);
+                continue;
+            }
+            // multicast: replica 0's items go through the multicast VA (one NVLink
+            // egress copy for all replicas); the other replicas' tiles emit nothing
+            if (rep != 0) continue;
+            std::vector<Item> tmp;
+            add_cast_items(t, tmp);
+            for (Item it : tmp) {
+                const int64_t n = int64_t(it.rows) * it.cols;
+                {
+                    it.flags = uint16_t(it.flags | F_MC);
+                    lists[sd][dd][grp].push_back(it);
+                    P->dev[size_t(sd)].has_mc = true;
+                    account(sd, sd, dd, n * es_src, n * es_dst, false);
+                    for (int d = 1; d < D->dp_gen; d++) {
+                        const int rd = P->dst_device[size_t(d * n_pos() + pos)];
+                        P->dev[size_t(rd)].hbm_write += n * es_dst;
+                        if (rd != sd) P->dev[size_t(rd)].nvl_rx += n * es_dst;
+                        P->traffic[size_t(sd) * P->n_devices + rd] += n * es_dst;
+                        P->stats.dst_bytes += n * es_dst;
+                        if (rd != sd) {
+                            auto &ex = mc_extra[size_t(sd)][grp];
+                            if (std::find(ex.begin(), ex.end(), rd) == ex.end()) ex.push_back(rd);
+                        }
+                    }
+                }
+            }
         }
         // fp8 blocks: group quantised tiles by (dst rank, dst param)
         std::map<std::pair<int, int>, std::vector<size_t>> by_param;
@@ -358,6 +402,10 @@ struct Builder {
                     for (auto &it : L) tot += item_bytes(it);
                     cur.push_back({d, 0, tot, 0});
                     if (d != e) { W.group_signal[size_t(grp)].push_back(d); sends[size_t(d)] = 1; }
+                }
+                for (int d : mc_extra[size_t(e)][size_t(grp)]) {      // multicast replicas are written too
+                    auto &gs = W.group_signal[size_t(grp)];
+                    if (std::find(gs.begin(), gs.end(), d) == gs.end()) { gs.push_back(d); sends[size_t(d)] = 1; }
                 }
                 // rotate the start by the executing device so senders spread over receivers
                 if (!cur.empty()) std::rotate(cur.begin(), cur.begin() + size_t(e) % cur.size(), cur.end());
@@ -471,7 +519,6 @@ extern "C" {
 
 llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, const int *src_device,
                              const int *dst_device, uint32_t flags, llrl_plan **out) {
-    (void)flags;
     if (!src || !dst || !src_device || !dst_device || !out || !src->is_src || dst->is_src) {
         set_error("llrl_plan_create: invalid argument");
         return LLRL_E_INVALID;
@@ -484,6 +531,7 @@ llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, con
     if (!P) { set_error("out of host memory"); return LLRL_E_NOMEM; }
     P->n_src = src->n_ranks;
     P->n_dst = dst->n_ranks;
+    P->multicast = (flags & LLRL_PLAN_MULTICAST) != 0;
     P->src_dtype = src->dtype;
     P->dst_dtype = dst->dtype;
     P->src_device.assign(src_device, src_device + P->n_src);

@@ -73,6 +73,7 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     for (const Item &it : W.items)
         if (it.flags & F_MX) { W.variant = kCastTmaVariant; break; }        // MXFP8 lives in the TMA kernel only
+    if (W.has_mc) W.variant = 1;                                             // multicast stores: register kernel
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
     if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = atoi(v) ? 1 : 0;
@@ -135,7 +136,7 @@ void touched_ranks(const DeviceWork &W, std::vector<char> &src, std::vector<char
         } else {
             src[it.src_rank] = 1;
         }
-        dst[it.dst_rank] = 1;
+        if (!(it.flags & F_MC)) dst[it.dst_rank] = 1;   // multicast items use the MC VA
     }
 }
 
@@ -178,6 +179,13 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
     }
     llrl_status st = ensure_uploaded(p, device);
     if (st != LLRL_OK) return st;
+    if (W.has_mc) {
+        if (W.dst_mc.size() != size_t(p->n_dst)) {
+            set_error("llrl_sync: device %d multicasts but llrl_plan_set_multicast was not called", device);
+            return LLRL_E_NOPEER;
+        }
+        for (int g = 0; g < p->n_dst; g++) kp->dst_mc[g] = W.dst_mc[size_t(g)];
+    }
     kp->items = W.d_items;
     kp->segs = W.d_segs;
     kp->tma_refs = W.d_tma_refs;

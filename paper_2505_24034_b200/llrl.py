@@ -23,6 +23,7 @@ OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED, E_CUDA, E_NOPEER, E_NOM
 F32, BF16, FP8_E4M3, MXFP8 = 0, 1, 2, 3
 DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8}
 MESH_FSDP_INNER = 1
+PLAN_MULTICAST = 1
 (P_ATTN_NORM, P_Q, P_K, P_V, P_O, P_MLP_NORM, P_GATE, P_UP, P_DOWN, P_EMBED, P_FINAL_NORM, P_LM_HEAD,
  P_QKV, P_GATE_UP) = range(14)
 
@@ -32,7 +33,8 @@ EXPORTS = [
     "llrl_plan_num_runs", "llrl_plan_get_runs", "llrl_plan_stats_get", "llrl_plan_traffic",
     "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
     "llrl_comm_set_peer", "llrl_comm_timed_out", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
-    "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_last_error",
+    "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
+    "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error",
     "llrl_version",
 ]
 
@@ -104,6 +106,11 @@ _sig("llrl_plan_stats_get", [_vp, _P(PlanStats)])
 _sig("llrl_plan_traffic", [_vp, _P(_i64)])
 _sig("llrl_plan_device_bytes", [_vp, _int, _P(_i64), _P(_i64), _P(_i64), _P(_i64)])
 _sig("llrl_plan_device_info", [_vp, _int, _P(DeviceInfo)])
+_sig("llrl_mc_create", [_int, _i64, _P(_int), _P(_i64), _P(_vp)])
+_sig("llrl_mc_import", [_int, _int, _i64, _P(_vp)])
+_sig("llrl_mc_join", [_vp, _int, _P(_vp), _P(_vp)])
+_sig("llrl_mc_destroy", [_vp], None)
+_sig("llrl_plan_set_multicast", [_vp, _int, _P(_vp)])
 _sig("llrl_comm_create", [_int, _P(_vp)])
 _sig("llrl_comm_export", [_vp, ctypes.c_char_p])
 _sig("llrl_comm_import", [_vp, _int, ctypes.c_char_p])
@@ -187,12 +194,13 @@ def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", f
 class Plan:
     _h = None
 
-    def __init__(self, src: Layout, dst: Layout, src_device, dst_device):
+    def __init__(self, src: Layout, dst: Layout, src_device, dst_device, multicast=False):
         assert len(src_device) == src.n_ranks and len(dst_device) == dst.n_ranks
         h = _vp()
         sd = (_int * len(src_device))(*src_device)
         dd = (_int * len(dst_device))(*dst_device)
-        _check(_lib.llrl_plan_create(src.handle, dst.handle, sd, dd, 0, ctypes.byref(h)))
+        _check(_lib.llrl_plan_create(src.handle, dst.handle, sd, dd, PLAN_MULTICAST if multicast else 0,
+                                     ctypes.byref(h)))
         self._h = h
         self.n_src, self.n_dst = src.n_ranks, dst.n_ranks
         self.src_device, self.dst_device = list(src_device), list(dst_device)
@@ -221,6 +229,9 @@ class Plan:
         v = DeviceInfo()
         _check(_lib.llrl_plan_device_info(self._h, device, ctypes.byref(v)))
         return v
+
+    def set_multicast(self, device, dst_mc_ptrs):
+        _check(_lib.llrl_plan_set_multicast(self._h, device, _ptrs(dst_mc_ptrs)))
 
     def num_runs(self):
         n = _i64()
@@ -308,6 +319,40 @@ class Comm:
     def close(self):
         if self._h:
             _lib.llrl_comm_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class McBuf:
+    """One NVLS multicast object (llrl_mc_*)."""
+    _h = None
+
+    def __init__(self, handle, size):
+        self._h = handle
+        self.size = size
+
+    @staticmethod
+    def create(n_devices, nbytes):
+        h, fd, size = _vp(), _int(), _i64()
+        _check(_lib.llrl_mc_create(n_devices, nbytes, ctypes.byref(fd), ctypes.byref(size), ctypes.byref(h)))
+        return McBuf(h, size.value), fd.value
+
+    @staticmethod
+    def import_fd(fd, n_devices, size):
+        h = _vp()
+        _check(_lib.llrl_mc_import(fd, n_devices, size, ctypes.byref(h)))
+        return McBuf(h, size)
+
+    def join(self, device):
+        """-> (local unicast pointer, multicast pointer) on `device`."""
+        a, b = _vp(), _vp()
+        _check(_lib.llrl_mc_join(self._h, device, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self._h:
+            _lib.llrl_mc_destroy(self._h)
             self._h = None
 
     __del__ = close

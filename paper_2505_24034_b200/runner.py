@@ -45,7 +45,8 @@ class SyncJob:
     In a torch.distributed job the calling process owns device ``rank``; without
     one, the job must fit one device (n_gpus == 1)."""
 
-    def __init__(self, spec: JobSpec, device: int | None = None, seed: int = 0, fill: bool = True):
+    def __init__(self, spec: JobSpec, device: int | None = None, seed: int = 0, fill: bool = True,
+                 multicast: bool = False):
         self.spec = spec
         self.cfg = cfg = spec.cfg
         self.model = spec.model()
@@ -61,12 +62,18 @@ class SyncJob:
         self.S, self.D = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype,
                                        cfg.dst_dtype, cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
         self.src_dev, self.dst_dev = placement(cfg, spec.n_gpus)
-        self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev)
+        self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev, multicast=multicast)
         dev = torch.device("cuda", self.device)
         self.src = {r: torch.empty(self.S.rank_bytes(r), dtype=torch.uint8, device=dev)
                     for r in range(self.S.n_ranks) if self.src_dev[r] == self.device}
-        self.dst = {g: torch.empty(self.D.rank_bytes(g), dtype=torch.uint8, device=dev)
-                    for g in range(self.D.n_ranks) if self.dst_dev[g] == self.device}
+        self._mc = []
+        self.mc_ranks = set()
+        self.dst = {}
+        if multicast and self.world > 1:
+            self._setup_multicast()
+        for g in range(self.D.n_ranks):
+            if self.dst_dev[g] == self.device and g not in self.dst:
+                self.dst[g] = torch.empty(self.D.rank_bytes(g), dtype=torch.uint8, device=dev)
         self.stream = torch.cuda.current_stream(dev)
         if fill:
             self.fill(seed)
@@ -89,7 +96,8 @@ class SyncJob:
         self.comm = llrl.Comm(self.device)
         mine = exchange_meta(self.device, self.comm.export(),
                              {r: llrl.ipc_handle(t.data_ptr()) for r, t in self.src.items()},
-                             {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()})
+                             {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()
+                              if g not in self.mc_ranks})   # multicast buffers are reached via the MC VA
         allm = [None] * self.world
         dist.all_gather_object(allm, mine)
         opened = {}
@@ -103,6 +111,82 @@ class SyncJob:
         for dev, h in flags.items():
             self.comm.import_peer(dev, h)
         self._opened = [(b, 0) for b in opened.values()]
+        dist.barrier()
+
+    def mc_positions(self):
+        """Generator rank positions whose DP replicas sit on pairwise different GPUs
+        (the plan's multicast eligibility rule, R12 numbering q = d*NS + pos)."""
+        dp = self.cfg.dp_gen
+        ns = self.D.n_ranks // dp
+        out = []
+        for pos in range(ns):
+            devs = [self.dst_dev[d * ns + pos] for d in range(dp)]
+            if dp > 1 and len(set(devs)) == dp:
+                out.append(pos)
+        return out, ns
+
+    def _setup_multicast(self):
+        """NVLS multicast (NEXT f1): one multicast object per eligible position; rank 0
+        creates them and passes the POSIX fds over a Unix socket (SCM_RIGHTS); every
+        process joins with its GPU; replica GPUs use the bound memory as their
+        generator buffer."""
+        import socket
+        dist = _dist()
+        positions, ns = self.mc_positions()
+        if not positions:
+            return
+        name = f"\0llrl-mc-{os.environ.get('MASTER_PORT', '0')}-{os.getuid()}-{id(self.plan) & 0xffff}"
+        holder = [name]
+        dist.broadcast_object_list(holder, src=0)
+        name = holder[0]
+        sizes, fds, bufs = [], [], []
+        if self.rank == 0:
+            for pos in positions:
+                buf, fd = llrl.McBuf.create(self.world, self.D.rank_bytes(pos))
+                bufs.append(buf)
+                fds.append(fd)
+                sizes.append(buf.size)
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(name)
+            srv.listen(self.world)
+            dist.broadcast_object_list([sizes], src=0)
+            for _ in range(self.world - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"llrl"], fds)
+                conn.close()
+            srv.close()
+            for fd in fds:
+                os.close(fd)
+        else:
+            holder = [None]
+            dist.broadcast_object_list(holder, src=0)
+            sizes = holder[0]
+            conn = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            import time
+            for _ in range(200):
+                try:
+                    conn.connect(name)
+                    break
+                except OSError:
+                    time.sleep(0.05)
+            _, fds, _, _ = socket.recv_fds(conn, 16, len(positions))
+            conn.close()
+            for fd, size in zip(fds, sizes):
+                bufs.append(llrl.McBuf.import_fd(fd, self.world, size))
+                os.close(fd)
+        dst_mc = [0] * self.D.n_ranks
+        dev = torch.device("cuda", self.device)
+        for pos, buf in zip(positions, bufs):
+            local, mcva = buf.join(self.device)           # blocks until every GPU joined
+            for d in range(self.cfg.dp_gen):
+                q = d * ns + pos
+                dst_mc[q] = mcva
+                if self.dst_dev[q] == self.device:
+                    self.dst[q] = _wrap_device_ptr(local, self.D.rank_bytes(q), dev)
+                    self.mc_ranks.add(q)
+            self.mc_ranks.update(d * ns + pos for d in range(self.cfg.dp_gen))
+        self._mc = bufs
+        self.plan.set_multicast(self.device, dst_mc)
         dist.barrier()
 
     # -- the hot path ----------------------------------------------------------
@@ -131,6 +215,21 @@ class SyncJob:
             self.comm.close()
             self.comm = None
         self.plan.close()
+        self.dst = {}
+        for b in self._mc:
+            b.close()
+        self._mc = []
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ holder: a torch view of library-owned memory."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": (nbytes,), "typestr": "|u1", "version": 3}
+
+
+def _wrap_device_ptr(ptr, nbytes, device):
+    return torch.as_tensor(_CudaArray(ptr, nbytes), device=device)
 
 
 def exchange_meta(device, flag_handle, src_handles, dst_handles):

@@ -26,9 +26,12 @@ from synth import LayoutConfig  # noqa: E402
 from tests import harness  # noqa: E402
 
 
-def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2, dp=1, ppt=1, ppg=1):
+def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, seed=3, reps=2, dp=1, ppt=1, ppg=1,
+             multicast=False):
     cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement, inner, dp_gen=dp, pp_train=ppt, pp_gen=ppg)
-    job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False)
+    job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False, multicast=multicast)
+    if multicast:
+        assert job.mc_positions()[0], "expected multicast-eligible replicas"
     ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, inner, dp, ppt, ppg)
     for rep in range(reps):
         src = harness.host_src(ol, seed + rep)
@@ -118,6 +121,10 @@ def main():
     toy_case(runner, world, 2, 2, 2, "bf16", "fp8", "disjoint", dp=2)
     toy_case(runner, world, 2, 2, 8, "bf16", "bf16", "colocated", ppt=2)       # pipeline re-staging
     toy_case(runner, world, 3, 1, 2, "f32", "mxfp8", "disjoint", ppt=2, ppg=2, dp=2)
+    # NVLS multicast fan-out to DP replicas on different GPUs (NEXT f1)
+    toy_case(runner, world, world, 1, 1, "f32", "bf16", "colocated", dp=world, multicast=True)
+    toy_case(runner, world, 3, 1, 2, "bf16", "bf16", "colocated", dp=world // 2 if world >= 4 else 2,
+             multicast=True)
     if "--full" in sys.argv:
         for name in ("c2", "c3"):
             full_case(runner, world, name)
