@@ -45,7 +45,7 @@ class LayoutConfig:
     tp_gen: int
     src_dtype: str          # "f32" | "bf16"
     dst_dtype: str          # "f32" | "bf16" | "fp8"
-    placement: str          # "disjoint" | "colocated" | "rotated"
+    placement: str          # "disjoint" | "colocated" | "rotated" | "fanout"
     fsdp_inner: bool = False
     notes: str = ""
     dp_gen: int = 1         # generator data-parallel replicas (R12)
@@ -79,6 +79,10 @@ CONFIGS = {
     # NEXT f2: MX formats for the generator, as tcgen05 block-scaled MMA consumes them
     "c7": LayoutConfig("c7", "llama3-70b", 1, 8, 8, "bf16", "mxfp8", "colocated",
                        notes="70B bf16 TP=8 -> MXFP8 TP=8 (E4M3 + E8M0 per 1x32)"),
+    # NEXT f1 with NVLS multicast: more generator replicas than trainer GPUs, so the
+    # trainer's NVLink egress binds without multicast (3 copies) and not with it (1 copy).
+    "c9": LayoutConfig("c9", "llama3-8b", 1, 1, 1, "bf16", "bf16", "fanout", dp_gen=3,
+                       notes="8B bf16 trainer on GPU 0 -> 3 bf16 TP=1 DP replicas on GPUs 1..3 (multicast fan-out)"),
     # NEXT f4: decoupled pipeline parallelism -- a PP=2 trainer
     # (FSDP=2 x TP=2 per stage) re-staged into a PP-less TP=8 generator.
     "c8": LayoutConfig("c8", "llama3-70b", 2, 2, 8, "bf16", "bf16", "colocated", pp_train=2,
@@ -97,6 +101,8 @@ def placement(cfg: LayoutConfig, n_gpus: int):
     ns, nd = cfg.n_src, cfg.n_dst
     if n_gpus == 1:
         return [0] * ns, [0] * nd
+    if cfg.placement == "fanout":          # trainer on GPU 0, generator ranks over GPUs 1..G-1
+        return [0] * ns, [1 + g * (n_gpus - 1) // nd for g in range(nd)]
     if cfg.placement == "disjoint":
         half = n_gpus // 2
         return ([r * half // ns for r in range(ns)],
