@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_
 
 constexpr int kCastStageBytes = 32 * 1024;
 constexpr int kCastStages = 4;
-constexpr int kCastWorkers = 384;
+constexpr int kCastWorkers = 640;
 
 // Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
 // item, at most kCastStageBytes of source.  Same enumeration on both roles.
