@@ -365,7 +365,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6", "c7", "c8", "c9"])
+    ap.add_argument("--config", default="c2", choices=sorted(__import__("synth").CONFIGS))
     ap.add_argument("--impl", default="llrl", choices=["llrl", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

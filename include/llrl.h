@@ -22,7 +22,8 @@
  *     on error llrl_last_error() returns a thread-local message.  No C++
  *     exception or abort crosses the ABI.
  *   - Offsets in llrl_param_view are BYTES from the rank buffer base.  Offsets
- *     in llrl_run are ELEMENTS of that side's data dtype.
+ *     in llrl_run are ELEMENTS of that side's data dtype (MXFP4: 4-bit
+ *     elements, i.e. twice the byte offset).
  *   - Rank buffers must be 256-byte aligned device allocations owned by the
  *     caller.  The library owns layouts, plans and comms until *_destroy,
  *     including their device-side tables and flag buffers.
@@ -53,7 +54,9 @@ typedef enum {
 /* LLRL_MXFP8: OCP MX E4M3 elements with one E8M0 scale byte per 1x32 row
  * group (NEXT f2, "quantization (fp8 or fp4) on the inference side", P:145;
  * reading R13); scale grid [R, ceil(C/32)] bytes after each quantised weight. */
-typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3 } llrl_dtype;
+/* LLRL_MXFP4: OCP MX E2M1 elements (two per byte, even element in the low
+ * nibble) with one E8M0 scale byte per 1x32 row group (reading R15). */
+typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3, LLRL_MXFP4 = 4 } llrl_dtype;
 
 /* Llama-style decoder shapes (Llama-3.1 config.json fields [ext]). */
 typedef struct {
@@ -92,7 +95,7 @@ typedef struct {
  * Describe the trainer (src) and generator (dst) layouts of `m` for a trainer
  * mesh fsdp x tp_train (fsdp*tp_train ranks, R1-R3) and a generator with
  * tp_gen ranks (R4).  src_dtype in {F32, BF16}; dst_dtype in {F32 (only from
- * F32: identity/provenance mode), BF16, FP8_E4M3 (R7), MXFP8 (R13)}.
+ * F32: identity/provenance mode), BF16, FP8_E4M3 (R7), MXFP8 (R13), MXFP4 (R15)}.
  * Errors: INVALID (NULL, non-positive sizes), INDIVISIBLE, UNSUPPORTED.
  * Ownership: *src_out and *dst_out belong to the caller (llrl_layout_destroy). */
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,

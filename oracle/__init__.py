@@ -19,7 +19,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED = 0, -1, -2, -3, -4
 E_NOMEM, E_UNCOVERED, E_OVERLAP = -7, -8, -9
-DTYPES = {"f32": 0, "bf16": 1, "fp8": 2, "mxfp8": 3}
+DTYPES = {"f32": 0, "bf16": 1, "fp8": 2, "mxfp8": 3, "mxfp4": 4}
 
 
 def build(force: bool = False) -> str:
@@ -60,6 +60,8 @@ def lib():
         L.orc_fp8_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.orc_mx_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_mx4_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_e2m1_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         L.orc_num_src_params.argtypes, L.orc_num_src_params.restype = [M], ctypes.c_int
         L.orc_num_dst_params.argtypes, L.orc_num_dst_params.restype = [M], ctypes.c_int
         L.orc_src_param_info.argtypes = [M, ctypes.c_int, i64p, i64p, ip]
@@ -109,6 +111,22 @@ def mx_block(x: np.ndarray):
     q = np.empty(x.shape, dtype=np.uint8)
     s = np.zeros(1, dtype=np.uint8)
     lib().orc_mx_block(_ptr(x), x.size, _ptr(q), _ptr(s))
+    return q, int(s[0])
+
+
+def e2m1(vals_f32: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(vals_f32, dtype=np.float32)
+    out = np.empty(a.shape, dtype=np.uint8)
+    lib().orc_e2m1_array(_ptr(a), a.size, _ptr(out))
+    return out
+
+
+def mx4_block(x: np.ndarray):
+    """Quantise one MXFP4 block (<= 32 elements) -> (uint8 codes, one per element; E8M0 byte)."""
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1)
+    q = np.empty(x.shape, dtype=np.uint8)
+    s = np.zeros(1, dtype=np.uint8)
+    lib().orc_mx4_block(_ptr(x), x.size, _ptr(q), _ptr(s))
     return q, int(s[0])
 
 

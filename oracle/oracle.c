@@ -45,7 +45,7 @@
 #define ORC_E_OVERLAP -9      /* a generator byte would be written twice */
 #define ORC_E_NOMEM -7
 
-enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2, ORC_MXFP8 = 3 };
+enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2, ORC_MXFP8 = 3, ORC_MXFP4 = 4 };
 
 typedef struct {
     int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, with_embed;
@@ -130,6 +130,82 @@ static uint8_t e4m3_encode(double a, uint8_t sign)
     int E = (e - 1) + 7;                         /* biased exponent */
     int m = (int)((f * 2.0 - 1.0) * 8.0);        /* exact: 3-bit mantissa */
     return (uint8_t)(sign | (uint8_t)(E << 3) | (uint8_t)m);
+}
+
+/* |value| a (exact, double) -> E2M1 (FP4: bias 1, 2 exponent bits, 1 mantissa
+ * bit; magnitudes {0, 0.5, 1, 1.5, 2, 3, 4, 6}) code, RN-even, saturating at 6
+ * (cvt.rn.satfinite.e2m1x2 semantics; R15).  sign is 0 or 8. */
+static uint8_t e2m1_encode(double a, uint8_t sign)
+{
+    if (a == 0.0)
+        return sign;
+    if (a > 6.0)
+        return (uint8_t)(sign | 0x7);
+    double quantum;
+    if (a < 1.0) {
+        quantum = 0.5;                           /* subnormal grid m * 0.5 */
+    } else {
+        int e;
+        frexp(a, &e);                            /* a = f * 2^e, f in [0.5,1) */
+        quantum = ldexp(1.0, (e - 1) - 1);       /* 1 mantissa bit */
+    }
+    double q = a / quantum;
+    double n = floor(q);
+    double rem = q - n;
+    if (rem > 0.5 || (rem == 0.5 && fmod(n, 2.0) != 0.0))
+        n += 1.0;
+    double r = n * quantum;
+    if (r > 6.0)
+        r = 6.0;
+    if (r == 0.0)
+        return sign;
+    if (r < 1.0)
+        return (uint8_t)(sign | 0x1);            /* 0.5: exponent field 0, mantissa 1 */
+    int e;
+    double f = frexp(r, &e);                     /* r = f*2^e */
+    int E = (e - 1) + 1;                         /* biased exponent */
+    int m = (int)((f * 2.0 - 1.0) * 2.0);        /* exact: 1-bit mantissa */
+    return (uint8_t)(sign | (uint8_t)(E << 1) | (uint8_t)m);
+}
+
+uint8_t orc_e2m1_rn_satfinite(float v)
+{
+    uint32_t vb;
+    memcpy(&vb, &v, 4);
+    return e2m1_encode(fabs((double)v), (uint8_t)((vb >> 31) << 3));
+}
+
+void orc_e2m1_array(const float *in, int64_t n, uint8_t *out)
+{
+    for (int64_t i = 0; i < n; i++)
+        out[i] = orc_e2m1_rn_satfinite(in[i]);
+}
+
+/* One MXFP4 block (OCP MX v1.0 with E2M1 elements, reading R15): as
+ * orc_mx_block with emax_elem = 2 (E2M1's largest exponent): X =
+ * floor(log2 amax) - 2 clamped below at -127; q = e2m1_rn_satfinite(v / 2^X)
+ * (exact quotient, one rounding); one code per output byte (the caller packs
+ * two per byte, even element in the low nibble). */
+void orc_mx4_block(const float *x, int64_t n, uint8_t *q, uint8_t *scale)
+{
+    float amax = 0.0f;
+    for (int64_t i = 0; i < n; i++)
+        if (fabsf(x[i]) > amax)
+            amax = fabsf(x[i]);
+    int X = -127;
+    if (amax > 0.0f) {
+        int e;
+        frexp((double)amax, &e);
+        X = (e - 1) - 2;
+        if (X < -127)
+            X = -127;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        uint32_t vb;
+        memcpy(&vb, &x[i], 4);
+        q[i] = e2m1_encode(fabs(ldexp((double)x[i], -X)), (uint8_t)((vb >> 31) << 3));
+    }
+    *scale = (uint8_t)(X + 127);
 }
 
 /* One MXFP8 block (OCP Microscaling Formats v1.0, E4M3 elements; DESIGN.md
@@ -298,12 +374,17 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0 || c->dp_gen <= 0 ||
         c->pp_train <= 0 || c->pp_gen <= 0)
         return ORC_E_INVALID;
+    /* R15: MXFP4 packs two elements per byte: every quantised generator tensor has
+     * an even number of columns (and, for whole 1x32 groups, a multiple of 32) */
+    if (c->dst_dtype == ORC_MXFP4 && (m->d_model % 32 || (m->n_heads * m->head_dim / c->tp_gen) % 32 ||
+                                      (m->d_ffn / c->tp_gen) % 32))
+        return ORC_E_UNSUPPORTED;
     /* R14: whole layers per stage */
     if (m->n_layers % c->pp_train || m->n_layers % c->pp_gen)
         return ORC_E_INDIVISIBLE;
     if (c->src_dtype != ORC_F32 && c->src_dtype != ORC_BF16)
         return ORC_E_UNSUPPORTED;
-    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_MXFP8)
+    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_MXFP4)
         return ORC_E_UNSUPPORTED;
     if (c->dst_dtype == ORC_F32 && c->src_dtype != ORC_F32)
         return ORC_E_UNSUPPORTED;
@@ -480,7 +561,7 @@ static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int stage, int
     default:
         return -1;
     }
-    if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8)
+    if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8 && c->dst_dtype != ORC_MXFP4)
         *quant = 0;
     if (stage >= 0 && layer_stage(m, layer, gs != G_EMBED, c->pp_gen) != stage) {
         *rows = 0; *cols = 0;          /* R14: not on this generator stage */
@@ -491,11 +572,20 @@ static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int stage, int
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+/* Bytes of a generator tensor's data: fp32 4, bf16 2, fp8 / MXFP8 1 per
+ * element; MXFP4 two elements per byte (R15; C even). */
+static int64_t data_bytes(const orc_cfg *c, int64_t R, int64_t C, int qt)
+{
+    if (qt)
+        return c->dst_dtype == ORC_MXFP4 ? R * C / 2 : R * C;
+    return R * C * (c->dst_dtype == ORC_F32 ? 4 : 2);
+}
+
 /* Bytes of a quantised weight's scale grid (R9, R13): fp8 blocks: fp32
  * [ceil(R/128), ceil(C/128)]; MXFP8: E8M0 bytes [R, ceil(C/32)]. */
 static int64_t scale_grid_bytes(const orc_cfg *c, int64_t R, int64_t C)
 {
-    if (c->dst_dtype == ORC_MXFP8)
+    if (c->dst_dtype == ORC_MXFP8 || c->dst_dtype == ORC_MXFP4)
         return R * cdiv(C, 32);
     return cdiv(R, 128) * cdiv(C, 128) * 4;
 }
@@ -516,10 +606,9 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
         int64_t R, C; int qt;
         if (dst_parts(m, c, g, stage, q, &R, &C, &qt, parts) < 0)
             return ORC_E_INVALID;
-        int64_t es = qt ? 1 : (c->dst_dtype == ORC_F32 ? 4 : 2);
         off = align256(off);
         int64_t data_off = off;
-        off += R * C * es;
+        off += data_bytes(c, R, C, qt);
         int64_t s_off = -1;
         if (qt) {
             off = align256(off);
@@ -541,8 +630,7 @@ int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
         return 0;
     int64_t R, C, off, soff; int qt;
     orc_dst_param(m, c, g, P - 1, &R, &C, &qt, &off, &soff);
-    int64_t es = qt ? 1 : (c->dst_dtype == ORC_F32 ? 4 : 2);
-    int64_t end = off + R * C * es;
+    int64_t end = off + data_bytes(c, R, C, qt);
     if (qt)
         end = soff + scale_grid_bytes(c, R, C);
     return align256(end);
@@ -657,7 +745,19 @@ static int write_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
     }
     /* Step 3-4: cast and store */
     int rc = ORC_OK;
-    if (qt && c->dst_dtype == ORC_MXFP8) {
+    if (qt && c->dst_dtype == ORC_MXFP4) {
+        int64_t nsc = cdiv(C, 32);
+        if ((rc = mark_written(written, off, R * C / 2)) || (rc = mark_written(written, soff, R * nsc)))
+            goto out;
+        uint8_t codes[32];
+        for (int64_t r = 0; r < R; r++)
+            for (int64_t j = 0; j < nsc; j++) {
+                int64_t n = C - j * 32 < 32 ? C - j * 32 : 32;
+                orc_mx4_block(local + r * C + j * 32, n, codes, dst + soff + r * nsc + j);
+                for (int64_t k = 0; k < n; k += 2)   /* even element -> low nibble */
+                    dst[off + (r * C + j * 32 + k) / 2] = (uint8_t)(codes[k] | (codes[k + 1] << 4));
+            }
+    } else if (qt && c->dst_dtype == ORC_MXFP8) {
         int64_t nsc = cdiv(C, 32);
         if ((rc = mark_written(written, off, R * C)) || (rc = mark_written(written, soff, R * nsc)))
             goto out;

@@ -22,6 +22,7 @@ constexpr int kMxGroup = 32;       // R13
 void set_error(const char *fmt, ...);
 int64_t dtype_bytes(int dt);
 int64_t scale_grid_bytes(int dt, int64_t rows, int64_t cols);
+int64_t data_bytes(int dt, int64_t elems);   // MXFP4: elems / 2
 
 // A rectangle [r0, r1) x [c0, c1) of a full parameter tensor.
 struct Rect {
@@ -104,6 +105,7 @@ enum ItemFlag : uint16_t {
     F_DST_F32 = 2,     // destination dtype f32 (identity), else bf16 (K_CAST)
     F_MX = 4,          // K_CAST into MXFP8 codes (1 byte); aux = scale byte base (R13)
     F_MC = 8,          // K_CAST stored through the NVLS multicast VA of dst_rank's position (f1)
+    F_FP4 = 16,        // with F_MX: MXFP4 (E2M1 codes, two per byte; dst offsets in 4-bit elements) (R15)
 };
 
 // Device work item (48 bytes).  Offsets in elements of each side's dtype, except

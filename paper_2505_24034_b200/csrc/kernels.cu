@@ -219,6 +219,36 @@ __device__ __forceinline__ uint4 quant16(const uint4 *w, float inv) {
     return make_uint4(ow[0], ow[1], ow[2], ow[3]);
 }
 
+// 16 source elements (W words) -> 16 e2m1 codes, two per byte, the even
+// element in the low nibble (cvt.e2m1x2 puts its first operand in the high nibble).
+template <bool SRC_F32, int W>
+__device__ __forceinline__ uint2 quant16_e2m1(const uint4 *w, float inv) {
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+        const uint32_t q[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            if (SRC_F32) {
+                x[4 * j + e] = __uint_as_float(q[e]);
+            } else {
+                x[8 * j + 2 * e] = bf16_lo(q[e]);
+                x[8 * j + 2 * e + 1] = bf16_hi(q[e]);
+            }
+        }
+    }
+    uint32_t ow[2] = {0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint32_t b;
+        asm("{ .reg .b8 t; cvt.rn.satfinite.e2m1x2.f32 t, %1, %2; cvt.u32.u8 %0, t; }"
+            : "=r"(b)
+            : "f"(__fmul_rn(x[2 * i + 1], inv)), "f"(__fmul_rn(x[2 * i], inv)));
+        ow[i / 4] |= b << (8 * (i % 4));
+    }
+    return make_uint2(ow[0], ow[1]);
+}
+
 // Single-source block, thread t covers rows (t/8) + 32k, k < 4, columns
 // [(t%8)*16, +16).  Raw source words stay in registers between the amax pass
 // and the quantise pass (one HBM read per element).  FROM_SMEM: the block was
@@ -604,8 +634,9 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
             int rows_per, segs;
             const int nch = cast_chunks(it, es, &rows_per, &segs);
             const bool mx = it.flags & F_MX;
+            const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
-            const int des = mx ? 1 : cast ? 2 : es;
+            const int des = mx ? 1 : cast ? 2 : es;          // bytes per element (MXFP4: halved below)
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&full_bar[st], (n / kCastStages) & 1);
@@ -639,11 +670,13 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
                             amax = word_amax<SRC_F32>(w[j], amax);
                         }
                         amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-                        // shared exponent floor(log2 amax) - 8, clamped at -127: E8M0 code max(E - 8, 0)
-                        const int code = max(int(amax >> 23) - 8, 0);
+                        // shared exponent floor(log2 amax) - emax (8 for E4M3, 2 for E2M1),
+                        // clamped at -127: E8M0 code max(E - emax, 0)
+                        const int code = max(int(amax >> 23) - (fp4 ? 2 : 8), 0);
                         const float inv = __uint_as_float(uint32_t(254 - code) << 23);   // 2^-(code - 127)
                         if (live) {
-                            reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
+                            if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
+                            else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
                             if ((u & 1) == 0) {
                                 const int e0 = u * 16, r = e0 / c.nc, cc = e0 - r * c.nc;
                                 const int64_t o = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0 + cc;
@@ -655,9 +688,11 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
                     cast_workers_sync();
                 }
                 if (leader) {
-                    for (int r = 0; r < c.nr; r++)
-                        bulk_s2g(dbase + (it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0) * des,
-                                 out + r * c.nc * des, uint32_t(c.nc * des));
+                    for (int r = 0; r < c.nr; r++) {
+                        const int64_t e = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0;   // element offset
+                        if (fp4) bulk_s2g(dbase + e / 2, out + r * c.nc / 2, uint32_t(c.nc / 2));
+                        else bulk_s2g(dbase + e * des, out + r * c.nc * des, uint32_t(c.nc * des));
+                    }
                     bulk_commit();
                     // release the previous stage once its store has read shared memory
                     bulk_wait_read<1>();

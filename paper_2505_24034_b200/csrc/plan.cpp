@@ -111,7 +111,9 @@ struct Builder {
                         t.lr0 = part.lr0 + (I.r0 - F.r0);
                         t.lc0 = I.c0 - F.c0;
                         t.dst_ld = pc.cols;
-                        t.dst_off = pc.byte_off / es_d + t.lr0 * pc.cols + t.lc0;
+                        // element offset in the rank buffer (MXFP4: 4-bit elements)
+                        t.dst_off = (pc.dtype == LLRL_MXFP4 ? 2 * pc.byte_off : pc.byte_off / es_d) +
+                                    t.lr0 * pc.cols + t.lc0;
                         t.quant = pc.quantised;
                         P->tiles.push_back(t);
                     }
@@ -174,7 +176,8 @@ struct Builder {
     // sides, its whole length) start and end on 32-element group boundaries.
     llrl_status add_mx_items(const Tile &t) {
         const Piece &pc = D->pieces[size_t(t.dst_rank)][size_t(t.dst_param)];
-        const int64_t base = pc.byte_off;                 // codes are bytes: element == byte
+        const bool fp4 = pc.dtype == LLRL_MXFP4;
+        const int64_t base = fp4 ? 2 * pc.byte_off : pc.byte_off;   // element offset of the tensor
         const bool contiguous = t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld);
         const bool ok = (t.dst_off - base) % kMxGroup == 0 && (contiguous ? (t.rows * t.cols) % kMxGroup == 0
                                                                           : t.cols % kMxGroup == 0) &&
@@ -189,7 +192,7 @@ struct Builder {
         const SrcParam &sp = S->src_params[size_t(t.src_param)];
         auto &L = lists[size_t(sd)][size_t(dd)][size_t(group_of(sp.kind, sp.layer))];
         for (Item it : tmp) {
-            it.flags = uint16_t((it.flags & F_VEC) | F_MX);
+            it.flags = uint16_t((it.flags & F_VEC) | F_MX | (fp4 ? F_FP4 : 0));
             if (!(it.flags & F_VEC) || it.dst_off % kMxGroup != 0) {
                 set_error("MXFP8: unaligned cast item");
                 return LLRL_E_UNSUPPORTED;
@@ -198,7 +201,7 @@ struct Builder {
             L.push_back(it);
         }
         const int64_t n = t.rows * t.cols;
-        account(sd, sd, dd, n * es_src, n + n / kMxGroup, false);
+        account(sd, sd, dd, n * es_src, (fp4 ? n / 2 : n) + n / kMxGroup, false);
         return LLRL_OK;
     }
 
@@ -272,7 +275,7 @@ struct Builder {
         mc_extra.assign(size_t(G), std::vector<std::vector<int>>(size_t(n_groups)));
         seglists.assign(G, {});
         // bf16 / f32 tiles, and MXFP8 tiles (row-wise 1x32 groups ride on cast items, R13)
-        const bool mx = D->dtype == LLRL_MXFP8;
+        const bool mx = D->dtype == LLRL_MXFP8 || D->dtype == LLRL_MXFP4;
         for (const Tile &t : P->tiles) {
             if (t.quant && !mx) continue;
             if (t.quant) {
@@ -502,7 +505,7 @@ struct Builder {
             for (const Piece &pc : D->pieces[size_t(g)]) {
                 const DstParamDesc &dpd = D->dst_params[size_t(pc.param)];
                 auto &rg = P->dst_group_range[size_t(g)][size_t(group_of(dpd.kind, dpd.layer))];
-                widen(rg, pc.byte_off, pc.byte_off + pc.rows * pc.cols * dtype_bytes(pc.dtype));
+                widen(rg, pc.byte_off, pc.byte_off + data_bytes(pc.dtype, pc.rows * pc.cols));
                 if (pc.quantised) widen(rg, pc.scale_off, pc.scale_off + scale_grid_bytes(pc.dtype, pc.rows, pc.cols));
             }
         return LLRL_OK;

@@ -20,8 +20,8 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED, E_CUDA, E_NOPEER, E_NOMEM = 0, -1, -2, -3, -4, -5, -6, -7
-F32, BF16, FP8_E4M3, MXFP8 = 0, 1, 2, 3
-DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8}
+F32, BF16, FP8_E4M3, MXFP8, MXFP4 = 0, 1, 2, 3, 4
+DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8, "mxfp4": MXFP4}
 MESH_FSDP_INNER = 1
 PLAN_MULTICAST = 1
 (P_ATTN_NORM, P_Q, P_K, P_V, P_O, P_MLP_NORM, P_GATE, P_UP, P_DOWN, P_EMBED, P_FINAL_NORM, P_LM_HEAD,

@@ -103,3 +103,16 @@ def expected_mx_group(ol: oracle.Layout, seed, g, gp, r, j):
     if ol.src_dtype == "bf16":
         bits = bits << np.uint32(16)
     return oracle.mx_block(bits.view(np.float32))
+
+
+def expected_mx4_group(ol: oracle.Layout, seed, g, gp, r, j):
+    """(codes one per element, E8M0 byte) of MXFP4 group j of row r, from the oracle."""
+    R, C, q, off, soff = ol.dst_param(g, gp)
+    c0 = j * 32
+    n = min(32, C - c0)
+    p, row, col = ol.dst_element_source(g, gp, r, c0)
+    is_norm = ol.src_param_info(p)[2] == 2
+    bits = synth.weight_bits(seed, p, is_norm, ol.src_dtype, np.array([row]), np.arange(col, col + n)).astype(np.uint32)
+    if ol.src_dtype == "bf16":
+        bits = bits << np.uint32(16)
+    return oracle.mx4_block(bits.view(np.float32))

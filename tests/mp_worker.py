@@ -112,6 +112,7 @@ def main():
         (2, 2, 8, "bf16", "fp8", "rotated"),
         (3, 2, 4, "f32", "f32", "disjoint"),
         (2, 2, 8, "bf16", "mxfp8", "rotated"),
+        (2, 2, 8, "f32", "mxfp4", "colocated"),
     ]
     for c in cases:
         toy_case(runner, world, *c)

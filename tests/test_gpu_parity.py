@@ -70,7 +70,7 @@ def test_fill_matches_synth(rt):
 
 
 SWEEP = [(f, tt, tg, sdt, ddt) for f in (1, 2, 3, 8) for tt in (1, 2, 4) for tg in (1, 2, 4, 8)
-         for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp8"))]
+         for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp8"), ("f32", "mxfp4"))]
 
 
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", SWEEP)
@@ -89,6 +89,8 @@ def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
     (1, 8, 8, "f32", "fp8", False),
     (3, 1, 4, "f32", "mxfp8", False),   # MXFP8 (R13)
     (2, 2, 8, "bf16", "mxfp8", True),
+    (3, 1, 4, "bf16", "mxfp4", False),  # MXFP4 (R15)
+    (2, 2, 8, "f32", "mxfp4", True),
 ])
 def test_toy_parity_odd(rt, fsdp, tpt, tpg, sdt, ddt, inner):
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, inner)
@@ -117,7 +119,7 @@ def _inject_specials(ol, src):
 
 
 @pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16"),
-                                     ("f32", "mxfp8"), ("bf16", "mxfp8")])
+                                     ("f32", "mxfp8"), ("bf16", "mxfp8"), ("f32", "mxfp4"), ("bf16", "mxfp4")])
 def test_toy_parity_special_values(rt, sdt, ddt):
     # tp_train = 1: no replicated trainer pieces, so injected values stay consistent
     job = _toy_job(rt, "toy", 3, 1, 4, sdt, ddt)
@@ -182,6 +184,17 @@ def _sampled_check(job, n_samples=20000, n_blocks=6, seed=0):
             got = got.view(np.uint32 if es == 4 else np.uint16).astype(np.int64)
             want = harness.expected_elements(ol, 0, g, gp, lr, lc)
             assert np.array_equal(got, want), (g, gp)
+        if cfg.dst_dtype == "mxfp4":
+            qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
+            for gp in rng.choice(qparams, n_blocks, replace=False):
+                R, C, q, off, soff = ol.dst_param(g, int(gp))
+                nsc = -(-C // 32)
+                for r, j in [(0, 0), (R - 1, nsc - 1), (int(rng.integers(R)), int(rng.integers(nsc)))]:
+                    codes, sw = harness.expected_mx4_group(ol, 0, g, int(gp), r, j)
+                    b0 = off + (r * C + j * 32) // 2
+                    got = t[b0:b0 + codes.size // 2].cpu().numpy()
+                    assert np.array_equal(got, (codes[0::2] | (codes[1::2] << 4)).astype(np.uint8)), (g, gp, r, j)
+                    assert int(t[soff + r * nsc + j].item()) == sw, (g, gp, r, j)
         if cfg.dst_dtype == "mxfp8":
             qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
             for gp in rng.choice(qparams, n_blocks, replace=False):
@@ -241,6 +254,15 @@ def test_full_c7_70b_mxfp8_sampled(rt):
     job.close()
 
 
+def test_full_c10_70b_mxfp4_sampled(rt):
+    """C10 (70B bf16 TP=8 -> MXFP4 TP=8, NEXT f2 fp4) at G=1, 40-layer slice."""
+    job = _full_job(rt, "c10")
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=4000, n_blocks=4)
+    job.close()
+
+
 def test_full_c3_70b_bf16_sampled(rt):
     """C3 (70B bf16 FSDP=8 -> bf16 TP=8) at G=1, 8-layer slice (memory)."""
     job = _full_job(rt, "c3", n_layers=8)
@@ -293,7 +315,7 @@ def test_toy_parity_sync_group(rt, sdt, ddt, f, tt, tg):
 
 
 @pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8),
-                                           ("bf16", "mxfp8", 2, 2, 8)])
+                                           ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8)])
 def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
     """llrl_sync_host: pinned host trainer shards in, host generator shards out,
     pipelined per layer group; twice, to exercise stream/event reuse."""

@@ -154,6 +154,50 @@ def test_mx_block_vs_numpy_ml_dtypes(oracle_lib, kind):
         assert (qb[:, 0] & 0x7F == 0x7E).all()        # 1.96875 * 2^8 = 504 -> satfinite 448
 
 
+def _e2m1_chunk(start, n):
+    x = (np.arange(n, dtype=np.uint64) + np.uint64(start)).astype(np.uint32)
+    f = x.view(np.float32)
+    f = f[np.isfinite(f)]
+    return int((oracle.e2m1(f) != f.astype(ml_dtypes.float4_e2m1fn).view(np.uint8)).sum())
+
+
+def test_e2m1_exhaustive_below_8_vs_ml_dtypes(oracle_lib):
+    """E2M1 (R15): every fp32 with |x| < 8 (both signs) against ml_dtypes
+    float4_e2m1fn (RNE, saturating at 6), plus the closed-form grid."""
+    limit = int(np.array([8.0], np.float32).view(np.uint32)[0])
+    n = 1 << 24
+    starts = list(range(0, limit, n)) + list(range(0x80000000, 0x80000000 + limit, n))
+    with cf.ThreadPoolExecutor(8) as ex:
+        assert sum(ex.map(lambda s: _e2m1_chunk(s, n), starts)) == 0
+    f = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0, 7.0, 1e30, -0.25, 0.5, 6.0], np.float32)
+    assert oracle.e2m1(f).tolist() == [0, 2, 2, 4, 4, 6, 6, 7, 7, 8, 1, 7]
+
+
+@pytest.mark.parametrize("kind", ["random", "wide_range", "zero", "saturating", "partial"])
+def test_mx4_block_vs_numpy_ml_dtypes(oracle_lib, kind):
+    rng = np.random.default_rng(12)
+    n = 32
+    if kind == "random":
+        x = rng.normal(0, 0.02, (64, n)).astype(np.float32)
+    elif kind == "wide_range":
+        x = (rng.normal(0, 1, (64, n)) * 10.0 ** rng.uniform(-37, 37, (64, 1))).astype(np.float32)
+    elif kind == "zero":
+        x = np.zeros((4, n), np.float32)
+    elif kind == "saturating":   # amax mantissa >= 1.5: largest elements scale into (6, 8)
+        x = rng.uniform(-1, 1, (64, n)).astype(np.float32)
+        x[:, 0] = np.float32(1.875)
+    else:
+        n = 20
+        x = rng.normal(0, 0.02, (8, n)).astype(np.float32)
+    packed, sb = brute.mx4_quant(x)
+    for r in range(x.shape[0]):
+        q, sc = oracle.mx4_block(x[r])
+        assert sc == sb[r, 0]
+        qq = np.zeros(n + (n & 1), np.uint8)
+        qq[:n] = q
+        assert np.array_equal((qq[0::2] | (qq[1::2] << 4)).astype(np.uint8), packed[r])
+
+
 # --------------------------------------------------------------------------- layout / sync
 
 def _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src, sentinel=0):
@@ -194,6 +238,8 @@ def test_oracle_vs_brute_toy_sweep_bf16(oracle_lib, fsdp, tpt, tpg):
     (3, 1, 4, "f32", "mxfp8", False),     # MXFP8 (R13)
     (2, 2, 8, "bf16", "mxfp8", True),
     (1, 8, 8, "bf16", "mxfp8", False),
+    (3, 1, 4, "f32", "mxfp4", False),     # MXFP4 (R15)
+    (2, 2, 8, "bf16", "mxfp4", True),
 ])
 def test_oracle_vs_brute_odd_layouts(oracle_lib, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]

@@ -40,7 +40,8 @@ def test_library_exports_every_declared_symbol(L):
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
     (f, tt, tg, "f32", "bf16", False) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)
 ] + [(2, 2, 8, "bf16", "fp8", True), (3, 1, 4, "f32", "fp8", False), (3, 2, 4, "f32", "f32", False),
-      (3, 1, 4, "f32", "mxfp8", False), (2, 2, 8, "bf16", "mxfp8", True)])
+      (3, 1, 4, "f32", "mxfp8", False), (2, 2, 8, "bf16", "mxfp8", True), (3, 1, 4, "f32", "mxfp4", False),
+      (2, 2, 8, "bf16", "mxfp4", True)])
 def test_layout_matches_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]
     S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, inner)
@@ -134,6 +135,7 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
     dst = [np.zeros(n, np.uint8) for n in dst_sizes]
     # fp8: assemble generator-local fp32 tensors, then quantise per 128x128 block
     local = {}
+    epb = 2 if dst_dtype == "mxfp4" else 1          # quantised elements per byte
     for r in runs:
         src = src_bufs[r["src_rank"]]
         raw = src[r["src_off"] * es:(r["src_off"] + r["len"]) * es]
@@ -141,7 +143,7 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
         g = r["dst_rank"]
         if r["flags"] & 1:
             local.setdefault(g, {})
-            buf = local[g].setdefault("codes", np.full(dst_sizes[g], np.nan, np.float32))
+            buf = local[g].setdefault("codes", np.full(dst_sizes[g] * epb, np.nan, np.float32))
             buf[r["dst_off"]:r["dst_off"] + r["len"]] = x
         elif dst_dtype == "f32":
             dst[g][r["dst_off"] * 4:(r["dst_off"] + r["len"]) * 4] = x.view(np.uint8)
@@ -152,9 +154,11 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
             v = D.param_view(g, gp)
             if not v.quantised:
                 continue
-            x = d["codes"][v.byte_off:v.byte_off + v.rows * v.cols].reshape(v.rows, v.cols)
+            e0 = v.byte_off * epb
+            x = d["codes"][e0:e0 + v.rows * v.cols].reshape(v.rows, v.cols)
             assert not np.isnan(x).any()
-            q, s = brute.mx_quant(x) if dst_dtype == "mxfp8" else brute.fp8_quant(x)
+            quant = {"mxfp8": brute.mx_quant, "mxfp4": brute.mx4_quant}.get(dst_dtype, brute.fp8_quant)
+            q, s = quant(x)
             dst[g][v.byte_off:v.byte_off + q.size] = q.reshape(-1)
             dst[g][v.scale_off:v.scale_off + s.nbytes] = s.view(np.uint8).reshape(-1)
     return dst
@@ -171,6 +175,8 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
     (3, 1, 4, "f32", "mxfp8", False, 2),
     (2, 2, 8, "bf16", "mxfp8", True, 4),
     (8, 1, 8, "bf16", "mxfp8", False, 8),
+    (3, 1, 4, "f32", "mxfp4", False, 2),
+    (2, 2, 8, "bf16", "mxfp4", True, 4),
 ])
 def test_plan_runs_reproduce_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner, G):
     m = MODELS["toy"]
