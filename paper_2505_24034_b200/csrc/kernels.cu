@@ -176,20 +176,27 @@ __device__ __forceinline__ void fp8_scales(uint32_t amax_bits, float *inv, float
     *scale = __fdiv_rn(amax_c, 448.0f);
 }
 
-// |x| bit patterns of one 16-byte word of source elements, max-accumulated.
+// |x| bit patterns of one 16-byte word of source elements, max-accumulated
+// (as fp32 bit patterns: order-preserving for non-negative values).  bf16
+// words: |x| on both halves with one mask, pairwise max.bf16x2, then the two
+// halves -- about one instruction per element.
+__device__ __forceinline__ uint32_t max_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 template <bool SRC_F32>
 __device__ __forceinline__ uint32_t word_amax(uint4 w, uint32_t amax) {
-    const uint32_t q[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int e = 0; e < 4; e++) {
-        if (SRC_F32) {
-            amax = max(amax, q[e] & 0x7FFFFFFFu);
-        } else {
-            amax = max(amax, (q[e] << 16) & 0x7FFFFFFFu);
-            amax = max(amax, q[e] & 0x7FFF0000u);
-        }
+    if (SRC_F32) {
+        amax = max(amax, w.x & 0x7FFFFFFFu);
+        amax = max(amax, w.y & 0x7FFFFFFFu);
+        amax = max(amax, w.z & 0x7FFFFFFFu);
+        return max(amax, w.w & 0x7FFFFFFFu);
     }
-    return amax;
+    constexpr uint32_t m = 0x7FFF7FFFu;
+    const uint32_t p = max_bf16x2(max_bf16x2(w.x & m, w.y & m), max_bf16x2(w.z & m, w.w & m));
+    return max(amax, max(p << 16, p & 0xFFFF0000u));
 }
 
 // 16 source elements (W words) -> 16 e4m3 codes (one 16-byte word).
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_
 
 constexpr int kCastStageBytes = 32 * 1024;
 constexpr int kCastStages = 4;
-constexpr int kCastWorkers = 640;
+constexpr int kCastWorkers = 512;
 
 // Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
 // item, at most kCastStageBytes of source.  Same enumeration on both roles.
@@ -558,19 +565,24 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cast_workers_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kCastWorkers) : "memory"); }
 
 template <bool SRC_F32>
-__global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {
+    // warp 0: producer (bulk loads global -> shared), warp 1: storer (bulk stores
+    // shared -> global), warps 2..: workers (conversion in shared memory).  A stage
+    // moves full (producer -> workers) -> converted (workers -> storer) -> empty
+    // (storer -> producer, once its bulk store has read the stage).
     constexpr int es = SRC_F32 ? 4 : 2;
-    extern __shared__ __align__(128) unsigned char stages[];   // kCastStages x (in 32 KiB [+ out 16 KiB])
-    constexpr int kOut = kCastStageBytes / 2;   // bf16 or MXFP8 codes of a chunk
+    constexpr int kWorkerWarps = kCastWorkers / 32;
+    extern __shared__ __align__(128) unsigned char stages[];   // kCastStages x (in 32 KiB + out 16 KiB)
+    constexpr int kOut = kCastStageBytes / 2;   // bf16, MXFP8 or MXFP4 codes of a chunk
     constexpr int kStride = kCastStageBytes + kOut;
-    __shared__ __align__(8) uint64_t full_bar[kCastStages], empty_bar[kCastStages];
+    __shared__ __align__(8) uint64_t full_bar[kCastStages], conv_bar[kCastStages], empty_bar[kCastStages];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kCastStages; s++) {
             mbar_init(&full_bar[s], 1);
+            mbar_init(&conv_bar[s], kWorkerWarps);
             mbar_init(&empty_bar[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -600,11 +612,48 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
                              uint32_t(c.nc * es), &full_bar[st]);
             }
         }
+    } else if (warp == 1) {
+        // storer: write each converted stage back, release it once read
+        int n = 0, pend = -1;
+        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+            const Item it = P.items[i];
+            int rows_per, segs;
+            const bool vec = it.flags & F_VEC;
+            const int nch = vec ? cast_chunks(it, es, &rows_per, &segs) : 1;
+            const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
+            const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
+            const int des = mx ? 1 : cast ? 2 : es;
+            char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
+                if (!vec) {                       // scalar item: workers wrote global memory directly
+                    if (lane == 0) mbar_arrive(&empty_bar[st]);
+                    continue;
+                }
+                if (lane == 0) {
+                    const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                    const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
+                    for (int r = 0; r < c.nr; r++) {
+                        const int64_t e = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0;   // element offset
+                        if (fp4) bulk_s2g(dbase + e / 2, out + r * c.nc / 2, uint32_t(c.nc / 2));
+                        else bulk_s2g(dbase + e * des, out + r * c.nc * des, uint32_t(c.nc * des));
+                    }
+                    bulk_commit();
+                    bulk_wait_read<1>();              // the previous group has read its stage
+                    if (pend >= 0) mbar_arrive(&empty_bar[pend]);
+                    pend = st;
+                }
+            }
+        }
+        if (lane == 0) {
+            bulk_wait_all();                      // every bulk store complete before the signal
+            if (pend >= 0) mbar_arrive(&empty_bar[pend]);
+        }
     } else {
-        // workers: (cast in smem), one thread stores each stage back with bulk copies
-        const int wt = threadIdx.x - 32;
-        const bool leader = wt == 0;
-        int n = 0, pend_stage = -1;
+        // workers
+        const int wt = threadIdx.x - 64;
+        int n = 0;
         for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
             const Item it = P.items[i];
             const bool dst_f32 = it.flags & F_DST_F32;
@@ -626,8 +675,8 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
                         *reinterpret_cast<uint16_t *>(dbase + dof * 2) = *reinterpret_cast<const uint16_t *>(src + so * 2);
                     }
                 }
-                cast_workers_sync();
-                if (leader) mbar_arrive(&empty_bar[st]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv_bar[st]);
                 n++;
                 continue;
             }
@@ -636,74 +685,56 @@ __global__ void __launch_bounds__(32 + kCastWorkers, 1) llrl_k_cast_tma(const __
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
-            const int des = mx ? 1 : cast ? 2 : es;          // bytes per element (MXFP4: halved below)
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&full_bar[st], (n / kCastStages) & 1);
-                const Chunk c = cast_chunk(it, es, rows_per, segs, k);
                 unsigned char *in = stages + st * kStride;
-                unsigned char *out = in;
-                if (cast) {
-                    out = in + kCastStageBytes;
-                    const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
-                    for (int u = wt; u < nunits; u += kCastWorkers) {
-                        const uint4 a = reinterpret_cast<const uint4 *>(in)[u];
-                        reinterpret_cast<uint2 *>(out)[u] =
-                            make_uint2(bf16x2_rn(__uint_as_float(a.x), __uint_as_float(a.y)),
-                                       bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    cast_workers_sync();
-                } else if (mx) {
-                    // MXFP8 (R13): lanes (2j, 2j+1) hold the two halves of one 1x32 group
-                    out = in + kCastStageBytes;
-                    const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
-                    for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
-                        const int u = u0 + wt;
-                        const bool live = u < nunits;
-                        constexpr int W = SRC_F32 ? 4 : 2;
-                        uint4 w[W];
-                        uint32_t amax = 0;
-#pragma unroll
-                        for (int j = 0; j < W; j++) {
-                            w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
-                            amax = word_amax<SRC_F32>(w[j], amax);
+                unsigned char *out = in + kCastStageBytes;
+                if (cast || mx) {
+                    const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                    if (cast) {
+                        const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
+                        for (int u = wt; u < nunits; u += kCastWorkers) {
+                            const uint4 a = reinterpret_cast<const uint4 *>(in)[u];
+                            reinterpret_cast<uint2 *>(out)[u] =
+                                make_uint2(bf16x2_rn(__uint_as_float(a.x), __uint_as_float(a.y)),
+                                           bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
                         }
-                        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-                        // shared exponent floor(log2 amax) - emax (8 for E4M3, 2 for E2M1),
-                        // clamped at -127: E8M0 code max(E - emax, 0)
-                        const int code = max(int(amax >> 23) - (fp4 ? 2 : 8), 0);
-                        const float inv = __uint_as_float(uint32_t(254 - code) << 23);   // 2^-(code - 127)
-                        if (live) {
-                            if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
-                            else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
-                            if ((u & 1) == 0) {
-                                const int e0 = u * 16, r = e0 / c.nc, cc = e0 - r * c.nc;
-                                const int64_t o = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0 + cc;
-                                dbase[it.aux + o / kMxGroup] = static_cast<char>(code);
+                    } else {
+                        // MX (R13 / R15): lanes (2j, 2j+1) hold the two halves of one 1x32 group
+                        const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
+                        for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
+                            const int u = u0 + wt;
+                            const bool live = u < nunits;
+                            constexpr int W = SRC_F32 ? 4 : 2;
+                            uint4 w[W];
+                            uint32_t amax = 0;
+#pragma unroll
+                            for (int j = 0; j < W; j++) {
+                                w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
+                                amax = word_amax<SRC_F32>(w[j], amax);
+                            }
+                            amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+                            // shared exponent floor(log2 amax) - emax (8 for E4M3, 2 for E2M1),
+                            // clamped at -127: E8M0 code max(E - emax, 0)
+                            const int code = max(int(amax >> 23) - (fp4 ? 2 : 8), 0);
+                            const float inv = __uint_as_float(uint32_t(254 - code) << 23);   // 2^-(code - 127)
+                            if (live) {
+                                if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
+                                else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
+                                if ((u & 1) == 0) {
+                                    const int e0 = u * 16, r = e0 / c.nc, cc = e0 - r * c.nc;
+                                    const int64_t o = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0 + cc;
+                                    dbase[it.aux + o / kMxGroup] = static_cast<char>(code);
+                                }
                             }
                         }
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    cast_workers_sync();
                 }
-                if (leader) {
-                    for (int r = 0; r < c.nr; r++) {
-                        const int64_t e = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0;   // element offset
-                        if (fp4) bulk_s2g(dbase + e / 2, out + r * c.nc / 2, uint32_t(c.nc / 2));
-                        else bulk_s2g(dbase + e * des, out + r * c.nc * des, uint32_t(c.nc * des));
-                    }
-                    bulk_commit();
-                    // release the previous stage once its store has read shared memory
-                    bulk_wait_read<1>();
-                    if (pend_stage >= 0) mbar_arrive(&empty_bar[pend_stage]);
-                    pend_stage = st;
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv_bar[st]);
             }
-        }
-        if (leader) {
-            bulk_wait_all();                      // every bulk store complete before the signal
-            if (pend_stage >= 0) mbar_arrive(&empty_bar[pend_stage]);
         }
     }
     complete(P);
@@ -771,7 +802,7 @@ static void launch_shape(int mode, int variant, bool src_f32, int *threads, size
     *threads = kThreads;
     *smem = 0;
     if (mode == 0 && variant == kCastTmaVariant) {
-        *threads = 32 + kCastWorkers;
+        *threads = 64 + kCastWorkers;
         *smem = size_t(kCastStages) * (kCastStageBytes + kCastStageBytes / 2);
     }
     if (mode == 1 && variant != 0) {
