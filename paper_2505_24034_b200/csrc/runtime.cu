@@ -64,12 +64,10 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const int64_t n_cast = W.n_cast, n_fp8 = int64_t(W.items.size()) - W.n_cast;
-    // Cast kernel: TMA-staged (G->S->G bulk copies) when the device's work is
-    // HBM-bound; the register kernel (16-byte LDG/STG) when NVLink binds -- its
-    // peer stores measured ~3% faster than bulk stores over NVLink (profiles/).
-    const double t_hbm = double(W.hbm_read + W.hbm_write) / 6533.5e9;
-    const double t_nvl = double(std::max(W.nvl_tx, W.nvl_rx)) / 770e9;
-    W.variant = t_nvl > t_hbm ? 1 : kDefaultCastVariant;
+    // Cast kernel: TMA-staged (G->S->G bulk copies, local or peer) by default --
+    // with its dedicated storer warp it matched or beat the register kernel on
+    // every HBM- and NVLink-bound config measured (profiles/r01_y_bench_*).
+    W.variant = kDefaultCastVariant;
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     for (const Item &it : W.items)
         if (it.flags & F_MX) { W.variant = kCastTmaVariant; break; }        // MXFP8 lives in the TMA kernel only
