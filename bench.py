@@ -279,6 +279,8 @@ def run_llrl(args):
     if not args.no_e2e:
         e2e = _e2e(job, args)
 
+    comp = _nccl_comparator(job, args) if (args.comparator and args.gpus > 1) else None
+
     tot = job.plan.stats()
     tr = job.plan.traffic()
     wire = sum(tr[i][j] for i in range(len(tr)) for j in range(len(tr)) if i != j)
@@ -306,6 +308,8 @@ def run_llrl(args):
         }
         if e2e:
             line["e2e"] = e2e
+        if comp:
+            line["comparator"] = comp
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.config, cfg.model)
         print(json.dumps(line), flush=True)
@@ -351,6 +355,36 @@ def _e2e(job, args):
             "steps": steps, "api": "llrl_sync_host (C ABI, pinned host buffers)"}
 
 
+def _nccl_comparator(job, args):
+    """NCCL baseline for the same exchange: one all_to_all_single per step moving
+    exactly the plan's GPU x GPU byte matrix (already-cast, already-packed bytes;
+    a real NCCL solution would add a pack pass before and an unpack pass after)."""
+    import torch
+    import torch.distributed as dist
+    tr = job.plan.traffic()
+    me = job.device
+    send = [int(tr[me][d]) for d in range(args.gpus)]
+    recv = [int(tr[s][me]) for s in range(args.gpus)]
+    dev = torch.device("cuda", me)
+    inp = torch.empty(max(1, sum(send)), dtype=torch.uint8, device=dev)
+    out = torch.empty(max(1, sum(recv)), dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        dist.all_to_all_single(out[:sum(recv)], inp[:sum(send)], recv, send)
+    _barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 10))
+    e0.record()
+    for _ in range(steps):
+        dist.all_to_all_single(out[:sum(recv)], inp[:sum(send)], recv, send)
+    e1.record()
+    _barrier()
+    ms = _allmax(e0.elapsed_time(e1) / steps)
+    del inp, out
+    return {"nccl_alltoallv_ms": round(ms, 3), "steps": steps,
+            "what": "torch.distributed.all_to_all_single (NCCL) of the plan's byte matrix; transport only, "
+                    "no cast / relayout / pack / unpack"}
+
+
 def _ncu_traffic(config, n):
     """dram read+write bytes per launch from the committed ncu --set full summary, if any."""
     try:
@@ -373,6 +407,7 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="override decoder layers (profiling only)")
     ap.add_argument("--placement", default=None, choices=["disjoint", "colocated", "rotated", "fanout"])
     ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")
+    ap.add_argument("--comparator", action="store_true", help="also time an NCCL all-to-all-v of the same bytes")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -71,7 +71,7 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     for (const Item &it : W.items)
         if (it.flags & F_MX) { W.variant = kCastTmaVariant; break; }        // MXFP8 lives in the TMA kernel only
-    if (W.has_mc) W.variant = 1;                                             // multicast stores: register kernel
+    if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
     if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = atoi(v) ? 1 : 0;
