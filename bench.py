@@ -310,7 +310,7 @@ def run_llrl(args):
             line["e2e"] = e2e
         if comp:
             line["comparator"] = comp
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and args.gpus == 1:      # rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(args.config, cfg.model)
         print(json.dumps(line), flush=True)
     job.close()
