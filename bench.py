@@ -280,6 +280,7 @@ def run_llrl(args):
         e2e = _e2e(job, args)
 
     comp = _nccl_comparator(job, args) if (args.comparator and args.gpus > 1) else None
+    ovl = _overlap(job, args) if args.overlap else None
 
     tot = job.plan.stats()
     tr = job.plan.traffic()
@@ -310,6 +311,8 @@ def run_llrl(args):
             line["e2e"] = e2e
         if comp:
             line["comparator"] = comp
+        if ovl:
+            line["overlap"] = ovl
         if not args.no_cpu_baseline and args.gpus == 1:      # rank 0 at N=1 only
             line["cpu_baseline"] = cpu_baseline(args.config, cfg.model)
         print(json.dumps(line), flush=True)
@@ -353,6 +356,48 @@ def _e2e(job, args):
     d2h = int(_allsum(sum(t.numel() for t in host_dst.values())))
     return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": steps, "api": "llrl_sync_host (C ABI, pinned host buffers)"}
+
+
+def _overlap(job, args):
+    """NEXT f3: the sync of layer l streams out while the optimizer updates layer
+    l+1 (llrl_sync_group per layer group) vs optimizer-then-sync.  The optimizer
+    here is a synthetic pass over the trainer bytes of each layer (x * 1.0, one
+    read + one write: values unchanged)."""
+    import torch
+    opt_stream = torch.cuda.Stream(device=job.device)
+    n = job.plan.num_groups()
+    views = [job.src_group_views(g) for g in range(n)]
+
+    def opt(vs):
+        for v in vs:
+            v.mul_(1.0)
+
+    def timed(fn, steps=5):
+        fn()
+        _barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(job.stream)
+        for _ in range(steps):
+            fn()
+        e1.record(job.stream)
+        _barrier()
+        return _allmax(e0.elapsed_time(e1) / steps)
+
+    def opt_all():
+        with torch.cuda.stream(job.stream):
+            for g in range(n):
+                opt(views[g])
+
+    def sequential():
+        opt_all()
+        job.sync()
+
+    def overlapped():
+        job.overlapped_step(lambda vs: opt(vs), opt_stream)
+
+    return {"optimizer_only_ms": round(timed(opt_all), 3), "sync_only_ms": round(timed(job.sync), 3),
+            "sequential_ms": round(timed(sequential), 3), "overlapped_ms": round(timed(overlapped), 3),
+            "groups": n, "optimizer": "synthetic pass x*1.0 over each layer's trainer bytes (torch mul_)"}
 
 
 def _nccl_comparator(job, args):
@@ -408,6 +453,7 @@ def main():
     ap.add_argument("--placement", default=None, choices=["disjoint", "colocated", "rotated", "fanout"])
     ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")
     ap.add_argument("--comparator", action="store_true", help="also time an NCCL all-to-all-v of the same bytes")
+    ap.add_argument("--overlap", action="store_true", help="also time per-layer optimizer/sync overlap (f3)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -251,6 +251,10 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device,
  * processes must issue the same sequence of llrl_sync / llrl_sync_group calls;
  * running every group once is equivalent to one llrl_sync. */
 llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n);
+/* Byte range [*lo, *hi) of layer group `group` in rank `rank`'s buffer on the
+ * trainer (side 0) or generator (side 1) side; *lo = *hi = -1 if the rank holds
+ * nothing of that group.  Lets a caller update / consume one group at a time. */
+llrl_status llrl_plan_group_range(const llrl_plan *p, int side, int rank, int group, int64_t *lo, int64_t *hi);
 llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group,
                             void *const *src_ptrs, void *const *dst_ptrs, void *stream);
 

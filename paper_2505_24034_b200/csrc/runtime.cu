@@ -251,6 +251,18 @@ llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n) {
     return LLRL_OK;
 }
 
+llrl_status llrl_plan_group_range(const llrl_plan *p, int side, int rank, int group, int64_t *lo, int64_t *hi) {
+    if (!p || !lo || !hi || group < 0 || group >= p->n_groups || (side != 0 && side != 1) || rank < 0 ||
+        rank >= (side == 0 ? p->n_src : p->n_dst)) {
+        set_error("llrl_plan_group_range: invalid argument");
+        return LLRL_E_INVALID;
+    }
+    const auto &r = (side == 0 ? p->src_group_range : p->dst_group_range)[size_t(rank)][size_t(group)];
+    *lo = r.first;
+    *hi = r.second;
+    return LLRL_OK;
+}
+
 llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group, void *const *src_ptrs,
                             void *const *dst_ptrs, void *stream) {
     if (!p || group < 0 || group >= p->n_groups) { set_error("llrl_sync_group: invalid group"); return LLRL_E_INVALID; }

@@ -194,6 +194,35 @@ class SyncJob:
         s = stream if stream is not None else self.stream
         self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
+    def sync_group(self, group, stream=None):
+        s = stream if stream is not None else self.stream
+        self.plan.sync_group(self.comm, self.device, group, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+
+    def src_group_views(self, group):
+        """Views of this device's trainer bytes of one layer group (for an optimizer step)."""
+        dt = torch.float32 if self.cfg.src_dtype == "f32" else torch.bfloat16
+        out = []
+        for r, t in self.src.items():
+            lo, hi = self.plan.group_range(0, r, group)
+            if lo >= 0:
+                out.append(t[lo:hi].view(dt))
+        return out
+
+    def overlapped_step(self, opt_fn, opt_stream, stream=None):
+        """NEXT f3: per layer group, the optimizer (opt_fn(views) on opt_stream)
+        updates group g while llrl_sync_group streams group g-1 out: the sync of a
+        layer starts as soon as that layer's update is done."""
+        s = stream if stream is not None else self.stream
+        n = self.plan.num_groups()
+        opt_stream.wait_stream(s)
+        for g in range(n):
+            with torch.cuda.stream(opt_stream):
+                opt_fn(self.src_group_views(g))
+                ev = torch.cuda.Event()
+                ev.record(opt_stream)
+            s.wait_event(ev)
+            self.sync_group(g, s)
+
     def sync_host(self, host_src, host_dst, stream=None):
         """End-to-end entry: host trainer shards in, host generator shards out."""
         s = stream if stream is not None else self.stream

@@ -314,6 +314,26 @@ def test_toy_parity_sync_group(rt, sdt, ddt, f, tt, tg):
     job.close()
 
 
+@pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("bf16", "fp8")])
+def test_toy_parity_overlapped_step(rt, sdt, ddt):
+    """f3: per-layer optimizer pass (x * 1.0, values unchanged) overlapped with
+    llrl_sync_group streaming the previous layer == the plain sync."""
+    job = _toy_job(rt, "toy", 2, 2, 4, sdt, ddt)
+    ol = oracle.Layout(job.model, 2, 2, 4, sdt, ddt)
+    src = harness.host_src(ol, 55)
+    for r, t in job.src.items():
+        t.copy_(torch.from_numpy(src[r]))
+    for t in job.dst.values():
+        t.fill_(0x21)
+    opt_stream = torch.cuda.Stream()
+    job.overlapped_step(lambda vs: [v.mul_(1.0) for v in vs], opt_stream)
+    torch.cuda.synchronize()
+    want = harness.oracle_dst(ol, src, 0x21)
+    for g, t in job.dst.items():
+        assert np.array_equal(t.cpu().numpy(), want[g]), g
+    job.close()
+
+
 @pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8),
                                            ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8)])
 def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
