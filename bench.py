@@ -223,6 +223,8 @@ def run_llrl(args):
         import dataclasses
         spec = runner.JobSpec(dataclasses.replace(spec.cfg, placement=args.placement), spec.n_gpus, spec.n_layers)
     job = runner.SyncJob(spec, device=local, seed=0, multicast=args.multicast)
+    if args.max_ctas:
+        job.plan.set_max_ctas(job.device, args.max_ctas)
     cfg = job.cfg
     stream = job.stream
 
@@ -295,6 +297,7 @@ def run_llrl(args):
             "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": "synthetic (counter-based Llama-init-scale weights)",
             "config": {"workload": _workload_name(cfg, args.gpus), "model": cfg.model,
                        "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
+                       "max_ctas": args.max_ctas or "all SMs",
                        "multicast": bool(args.multicast and job.mc_positions()[0]),
                        "layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
@@ -454,6 +457,7 @@ def main():
     ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")
     ap.add_argument("--comparator", action="store_true", help="also time an NCCL all-to-all-v of the same bytes")
     ap.add_argument("--overlap", action="store_true", help="also time per-layer optimizer/sync overlap (f3)")
+    ap.add_argument("--max-ctas", type=int, default=0, help="cap the sync kernels' CTAs per GPU (0 = all SMs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

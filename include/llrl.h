@@ -269,6 +269,12 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device,
                            const void *const *host_src, void *const *host_dst,
                            void *const *src_ptrs, void *const *dst_ptrs, void *stream);
 
+/* Cap the CTAs (≈ SMs) the sync kernels of `device` use (0 = all).  An
+ * NVLink-bound device saturates its links with a fraction of the SMs, leaving
+ * the rest to overlapping compute (f3).  Must be called before the first sync
+ * on that device or between syncs (tables are re-uploaded). */
+llrl_status llrl_plan_set_max_ctas(llrl_plan *p, int device, int max_ctas);
+
 /* Number of kernels llrl_sync enqueues on `device` (for launch accounting). */
 llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n);
 

@@ -190,6 +190,7 @@ struct DeviceWork {
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
     int grid_cast = 0, grid_fp8 = 0;
     int variant = 0;                   // cast-kernel variant (kernels.cu)
+    int max_ctas = 0;                  // grid cap (0 = all SMs); llrl_plan_set_max_ctas
     int fp8_variant = 1;               // 0: register kernel, 1: TMA pipeline
 };
 

@@ -80,7 +80,9 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         CK(sync_occupancy(mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, &per_sm));
         if (per_sm < 1) per_sm = 1;
         const int64_t n = mode == 0 ? n_cast : n_fp8;
-        const int g = int(std::min<int64_t>(int64_t(sms) * per_sm, std::max<int64_t>(1, n)));
+        int64_t cap = int64_t(sms) * per_sm;
+        if (W.max_ctas > 0) cap = std::min<int64_t>(cap, W.max_ctas);           // llrl_plan_set_max_ctas
+        const int g = int(std::min<int64_t>(cap, std::max<int64_t>(1, n)));
         (mode == 0 ? W.grid_cast : W.grid_fp8) = g;
     }
     W.done_total = 0;
@@ -248,6 +250,20 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
 llrl_status llrl_plan_num_groups(const llrl_plan *p, int *n) {
     if (!p || !n) { set_error("NULL argument"); return LLRL_E_INVALID; }
     *n = p->n_groups;
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_set_max_ctas(llrl_plan *p, int device, int max_ctas) {
+    if (!p || device < 0 || device >= p->n_devices || max_ctas < 0) { set_error("invalid argument"); return LLRL_E_INVALID; }
+    DeviceWork &W = p->dev[size_t(device)];
+    W.max_ctas = max_ctas;
+    if (W.uploaded_device >= 0) {
+        DeviceGuard guard(device);
+        cudaFree(W.d_items); cudaFree(W.d_segs); cudaFree(W.d_done); cudaFree(W.d_tma_refs); cudaFree(W.d_tmaps);
+        W.d_items = nullptr; W.d_segs = nullptr; W.d_done = nullptr; W.d_tma_refs = nullptr; W.d_tmaps = nullptr;
+        W.tmap_src.clear();
+        W.uploaded_device = -1;
+    }
     return LLRL_OK;
 }
 

@@ -33,7 +33,7 @@ EXPORTS = [
     "llrl_plan_num_runs", "llrl_plan_get_runs", "llrl_plan_stats_get", "llrl_plan_traffic",
     "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
     "llrl_comm_set_peer", "llrl_comm_timed_out", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
-    "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_plan_group_range", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
+    "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_plan_group_range", "llrl_plan_set_max_ctas", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
     "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error",
     "llrl_version",
 ]
@@ -123,6 +123,7 @@ _sig("llrl_ipc_open", [ctypes.c_char_p, _i64, _P(_vp)])
 _sig("llrl_ipc_close", [_vp, _i64])
 _sig("llrl_sync", [_vp, _vp, _int, _P(_vp), _P(_vp), _vp])
 _sig("llrl_plan_num_groups", [_vp, _P(_int)])
+_sig("llrl_plan_set_max_ctas", [_vp, _int, _int])
 _sig("llrl_plan_group_range", [_vp, _int, _int, _int, _P(_i64), _P(_i64)])
 _sig("llrl_sync_group", [_vp, _vp, _int, _int, _P(_vp), _P(_vp), _vp])
 _sig("llrl_sync_host", [_vp, _vp, _int, _P(_vp), _P(_vp), _P(_vp), _P(_vp), _vp])
@@ -264,6 +265,9 @@ class Plan:
         n = _int()
         _check(_lib.llrl_plan_num_groups(self._h, ctypes.byref(n)))
         return n.value
+
+    def set_max_ctas(self, device, n):
+        _check(_lib.llrl_plan_set_max_ctas(self._h, device, n))
 
     def group_range(self, side, rank, group):
         lo, hi = _i64(), _i64()
