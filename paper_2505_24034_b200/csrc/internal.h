@@ -160,6 +160,8 @@ struct DeviceWork {
     std::vector<Seg> segs;
     std::vector<TmaRef> tma_refs;      // one per fp8 item (index i - n_cast)
     std::vector<void *> dst_mc;        // multicast VA per dst rank (llrl_plan_set_multicast)
+    std::vector<char> src_touched, dst_touched;   // ranks this device's items read / write
+    bool touched_valid = false;
     bool has_mc = false;
     std::vector<TmaPiece> tma_pieces;
     std::vector<int> signal_devices;   // devices this device writes into (excl. itself)

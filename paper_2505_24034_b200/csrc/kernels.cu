@@ -1,20 +1,26 @@
 // kernels.cu -- the hot path for sm_100a.
 //
-// K1 relayout + cast + move   (a3; §5.2: each GPU sends its
-//                               own shards straight into the generator's CUDA
-//                               memory over NVLink, no CPU, no PS hop)
-// K2 fp8 128x128 block quant  (a4; "quantization ... on the inference side",
-//                               P:145; arithmetic = DESIGN.md R7)
-// K3 completion               (a6; release/acquire epoch counters, R10)
+// K1  llrl_k_cast_tma  relayout + cast + move (a3; §5.2: each
+//                      GPU sends its own shards straight into the generator's
+//                      CUDA memory over NVLink, no CPU, no PS hop), plus the
+//                      MXFP8 / MXFP4 row-group quantisation (R13, R15).
+//                      Warp-specialised: a producer warp stages rows with
+//                      cp.async.bulk (TMA) into a 4-deep shared-memory ring,
+//                      worker warps convert in shared memory, a storer warp
+//                      writes back with bulk copies to local or peer HBM.
+// K1r llrl_k_cast<U,M> register variant of K1 (16-byte LDG / STG, U loads in
+//                      flight per thread); used for NVLS multicast stores (f1).
+// K2  llrl_k_fp8_tma   fp8 128x128 block quantisation (a4; R7): 2-D tensor-map
+//                      TMA box per block, warp-specialised like K1.
+// K2r llrl_k_fp8       register variant of K2.
+// K3  completion       (a6): last CTA of a launch publishes a release add to every
+//                      destination GPU's per-sender counter; llrl_k_wait spins
+//                      with acquire loads (R10).
 //
-// One persistent kernel per device and sync executes every work item that
-// device owns (push items for tiles it sources, pull items for multi-source fp8
-// blocks landing on it).  The work is a memory-movement problem with ~1 ALU op
-// per element: no tensor cores; the design targets HBM and NVLink bandwidth:
-// 16-byte vector loads (L1 no-allocate, read-only path) and 16-byte stores to
-// local or peer-mapped addresses, several independent loads in flight per
-// thread, and a grid of (#SMs x resident CTAs) CTAs striding over work items
-// that the planner interleaved across destinations.
+// The work is memory movement with about one ALU op per element: no dense
+// contraction, no tensor cores; the design targets HBM and NVLink bandwidth.
+// Every launch is a persistent grid (one CTA per SM for the TMA kernels)
+// striding over work items the planner interleaved across destinations.
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -836,7 +842,6 @@ cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStr
     return cudaGetLastError();
 }
 
-int sync_threads() { return kThreads; }
 
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm) {
     const void *fn = kernel_for(mode, variant, src_f32);

@@ -17,7 +17,7 @@ struct KParams {
     const void *tmaps;                 // CUtensorMap array (global memory)
     int fp8_base;
     unsigned long long *done;          // per (plan, device) CTA completion counter, or null
-    unsigned long long done_target;    // epoch * gridDim.x of the signalling launch
+    unsigned long long done_target;    // cumulative CTAs of all signalling launches (this one included)
     int item_begin, item_end;          // [begin, end) of this launch
     int n_signal;
     unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
@@ -40,7 +40,6 @@ cudaError_t launch_signal(const SignalTargets &t, cudaStream_t stream);
 cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream);
 cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_sm);
 int num_cast_variants();
-int sync_threads();
 
 // K0 (init.cu): synthetic trainer weights of one piece.
 struct FillPiece {

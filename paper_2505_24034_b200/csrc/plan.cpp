@@ -20,7 +20,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
-#include <numeric>
 
 #include "internal.h"
 
@@ -231,7 +230,6 @@ struct Builder {
         else P->traffic[size_t(exec) * G + ddev] += dst_bytes;
         P->stats.src_bytes += src_bytes;
         P->stats.dst_bytes += dst_bytes;
-        (void)exec;
     }
 
     // For every single-source vector fp8 block: the trainer piece it reads

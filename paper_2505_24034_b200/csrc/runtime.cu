@@ -129,15 +129,20 @@ llrl_status ensure_tmaps(llrl_plan *p, DeviceWork &W, void *const *src_ptrs, cud
 }
 
 // Which ranks a device's items touch (for pointer validation).
-void touched_ranks(const DeviceWork &W, std::vector<char> &src, std::vector<char> &dst) {
+// Which ranks a device's items touch (pointer validation); computed once.
+void touched_ranks(DeviceWork &W, int n_src, int n_dst) {
+    if (W.touched_valid) return;
+    W.src_touched.assign(size_t(n_src), 0);
+    W.dst_touched.assign(size_t(n_dst), 0);
     for (const Item &it : W.items) {
         if (it.kind == K_FP8_MULTI) {
-            for (int s = 0; s < it.src_rank; s++) src[size_t(W.segs[size_t(it.src_off) + s].src_rank)] = 1;
+            for (int s = 0; s < it.src_rank; s++) W.src_touched[size_t(W.segs[size_t(it.src_off) + s].src_rank)] = 1;
         } else {
-            src[it.src_rank] = 1;
+            W.src_touched[it.src_rank] = 1;
         }
-        if (!(it.flags & F_MC)) dst[it.dst_rank] = 1;   // multicast items use the MC VA
+        if (!(it.flags & F_MC)) W.dst_touched[it.dst_rank] = 1;   // multicast items use the MC VA
     }
+    W.touched_valid = true;
 }
 
 }  // namespace
@@ -166,8 +171,8 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
                 return LLRL_E_NOPEER;
             }
     }
-    std::vector<char> su(size_t(p->n_src), 0), du(size_t(p->n_dst), 0);
-    touched_ranks(W, su, du);
+    touched_ranks(W, p->n_src, p->n_dst);
+    const std::vector<char> &su = W.src_touched, &du = W.dst_touched;
     std::memset(kp, 0, sizeof *kp);
     for (int r = 0; r < p->n_src; r++) {
         if (su[size_t(r)] && !src_ptrs[r]) { set_error("llrl_sync: src_ptrs[%d] is NULL", r); return LLRL_E_NOPEER; }
