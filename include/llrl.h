@@ -179,10 +179,13 @@ typedef struct {
 llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
 
 /* ---- completion comm (a6) --------------------------------------------------
- * A comm owns one 512-byte flag buffer on `device`: word s counts data
- * arrivals from sender device s, word 16 + s counts "trainer bytes staged"
+ * A comm owns one 1 KiB flag buffer on `device`: word s counts data arrivals
+ * from sender device s, word 16 + s counts "trainer bytes staged"
  * announcements of device s (llrl_sync_host with pull items), word 32 is set
- * if a wait timed out (30 s).  All counters are cumulative.
+ * if a wait timed out (30 s), words 64.. hold the arrivals expected so far.
+ * All counters are cumulative and live on the device: llrl_sync /
+ * llrl_sync_group launch identical parameters on every call, so after one
+ * warm-up call they can be captured in a CUDA graph and replayed.
  * Devices that exchange data in a plan must know each other's flag buffers:
  *   multi-process: llrl_comm_export on each, exchange the 64-byte handles
  *                  (e.g. torch.distributed.all_gather_object), llrl_comm_import;

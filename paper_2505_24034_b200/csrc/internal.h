@@ -186,7 +186,6 @@ struct DeviceWork {
     std::vector<unsigned char> h_tmaps;     // host copy (kept alive for the async upload)
     std::vector<const void *> tmap_src;     // src base pointers the maps were encoded for
     unsigned long long *d_done = nullptr;   // last-CTA counter (cumulative)
-    uint64_t done_total = 0;                // CTAs of all signalling launches so far
     void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)
     std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
@@ -217,9 +216,9 @@ struct llrl_comm {
     int device;
     // flags[s]: data arrivals from sender device s; flags[kMaxDevices + s]:
     // "trainer bytes staged" announcements from device s (llrl_sync_host);
-    // flags[2 * kMaxDevices]: wait-timeout flag.  512 bytes.
+    // flags[2 * kMaxDevices]: wait-timeout flag; flags[4 * kMaxDevices + slot]:
+    // arrivals expected so far (device-side, local).  1 KiB.
     unsigned long long *flags = nullptr;
     unsigned long long *peer_flags[llrl::kMaxDevices] = {};
-    uint64_t expected[2 * llrl::kMaxDevices] = {};   // cumulative arrivals expected per slot
     bool ipc_opened[llrl::kMaxDevices] = {};
 };

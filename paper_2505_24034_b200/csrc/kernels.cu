@@ -363,15 +363,19 @@ __device__ void fp8_item_generic(const Item &it, const KParams &P, uint32_t *s_r
 // ---- the persistent sync kernel + K3 signal -------------------------------------
 
 // Completion (a6): every thread orders its stores at system scope, the CTA
-// joins, one thread counts the CTA in; the last CTA of the launch publishes one
-// arrival to every destination device with a release add at system scope.
+// joins, one thread counts the CTA in; the last CTA of the launch resets the
+// counter for the next launch on the stream and publishes one arrival to every
+// destination device with a release add at system scope.  No per-call host
+// state: the launch parameters are the same on every call, so a sync can be
+// captured once in a CUDA graph and replayed.
 __device__ __forceinline__ void complete(const KParams &P) {
     if (P.done == nullptr) return;
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned long long prev = atomicAdd(P.done, 1ULL);
-        if (prev + 1 == P.done_target) {
+        if (prev + 1 == gridDim.x) {
+            atomicExch(P.done, 0ULL);
             __threadfence_system();
             for (int s = 0; s < P.n_signal; s++)
                 asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(P.signal[s]) : "memory");
@@ -754,12 +758,16 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
 // timeout flag[2 * kMaxDevices] = 1.
 __global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned long long timeout_ns) {
     const int s = threadIdx.x;
-    if (s >= 2 * kMaxDevices || t.target[s] == 0) return;
+    if (s >= 2 * kMaxDevices || t.count[s] == 0) return;
+    // expected arrivals live on the device (flags[kExpected + s]): graph-replayable
+    unsigned long long *expected = flags + kFlagExpected + s;
+    const unsigned long long target = *expected + t.count[s];
+    *expected = target;
     unsigned long long t0, now, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + s) : "memory");
-        if (v >= t.target[s]) return;
+        if (v >= target) return;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         if (now - t0 > timeout_ns) {
             atomicExch(flags + 2 * kMaxDevices, 1ULL);

@@ -16,8 +16,7 @@ struct KParams {
     const TmaRef *tma_refs;            // fp8 items: index i - fp8_base
     const void *tmaps;                 // CUtensorMap array (global memory)
     int fp8_base;
-    unsigned long long *done;          // per (plan, device) CTA completion counter, or null
-    unsigned long long done_target;    // cumulative CTAs of all signalling launches (this one included)
+    unsigned long long *done;          // per (plan, device) CTA completion counter (self-resetting), or null
     int item_begin, item_end;          // [begin, end) of this launch
     int n_signal;
     unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
@@ -29,8 +28,14 @@ struct KParams {
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
 constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
+// comm flag buffer words: [0, 16) data arrivals per sender, [16, 32) staging
+// announcements per device, [32] timeout flag, [64, 96) expected counts
+// (device-side, local only).
+constexpr int kFlagTimeout = 2 * kMaxDevices;
+constexpr int kFlagExpected = 4 * kMaxDevices;
+constexpr int kFlagBytes = 8 * 8 * kMaxDevices;
 struct WaitTargets {
-    unsigned long long target[2 * kMaxDevices];   // per flag slot; 0 = do not wait
+    unsigned long long count[2 * kMaxDevices];   // arrivals to wait for per flag slot; 0 = none
 };
 struct SignalTargets {
     unsigned long long *slot[kMaxDevices];

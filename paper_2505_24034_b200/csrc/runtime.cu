@@ -85,7 +85,6 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         const int g = int(std::min<int64_t>(cap, std::max<int64_t>(1, n)));
         (mode == 0 ? W.grid_cast : W.grid_fp8) = g;
     }
-    W.done_total = 0;
     W.uploaded_device = device;
     return LLRL_OK;
 }
@@ -218,9 +217,7 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
         kp.done = nullptr;
         kp.n_signal = 0;
         if (last && !sig.empty()) {
-            W.done_total += uint64_t(grid);
             kp.done = W.d_done;
-            kp.done_target = W.done_total;
             kp.n_signal = int(sig.size());
             for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]] + comm->device;
         }
@@ -234,7 +231,7 @@ static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &devs, 
     if (devs.empty()) return LLRL_OK;
     WaitTargets t;
     std::memset(&t, 0, sizeof t);
-    for (int d : devs) t.target[base + d] = ++comm->expected[base + d];
+    for (int d : devs) t.count[base + d] = 1;
     CK(launch_wait(comm->flags, t, s));
     return LLRL_OK;
 }
@@ -421,8 +418,8 @@ llrl_status llrl_comm_create(int device, llrl_comm **out) {
     if (!c) { set_error("out of host memory"); return LLRL_E_NOMEM; }
     c->device = device;
     DeviceGuard guard(device);
-    cudaError_t e = cudaMalloc(&c->flags, 512);
-    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, 512);
+    cudaError_t e = cudaMalloc(&c->flags, kFlagBytes);
+    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, kFlagBytes);
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "llrl_comm_create"); }
     c->peer_flags[device] = c->flags;
     *out = c;
@@ -473,7 +470,7 @@ llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out) {
     if (!c || !timed_out) { set_error("invalid argument"); return LLRL_E_INVALID; }
     DeviceGuard guard(c->device);
     unsigned long long v = 0;
-    CK(cudaMemcpy(&v, c->flags + 2 * kMaxDevices, sizeof v, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v, c->flags + kFlagTimeout, sizeof v, cudaMemcpyDeviceToHost));
     *timed_out = v != 0;
     return LLRL_OK;
 }

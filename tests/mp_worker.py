@@ -76,6 +76,25 @@ def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, se
     for g in job.dst:
         assert np.array_equal(hd[g].numpy(), want[g]), f"{cfg} sync_host: dst rank {g}"
     assert job.comm is None or not job.comm.timed_out()
+    # CUDA-graph replay of the multi-GPU sync (device-side completion state)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        job.sync(stream=torch.cuda.current_stream())
+    for rep in range(2):
+        src = harness.host_src(ol, seed + 80 + rep)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x5A)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        want = harness.oracle_dst(ol, src, 0x5A)
+        for q, t in job.dst.items():
+            assert np.array_equal(t.cpu().numpy(), want[q]), f"{cfg} graph replay {rep}: dst rank {q}"
     job.close()
 
 

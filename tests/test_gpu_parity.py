@@ -334,6 +334,35 @@ def test_toy_parity_overlapped_step(rt, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp8")])
+def test_toy_parity_cuda_graph_replay(rt, sdt, ddt):
+    """Completion state lives on the device, so a warmed-up sync (and the per-layer
+    overlapped step) can be captured once in a CUDA graph and replayed."""
+    job = _toy_job(rt, "toy", 2, 2, 4, sdt, ddt)
+    ol = oracle.Layout(job.model, 2, 2, 4, sdt, ddt)
+    job.sync()                                   # warm-up: uploads tables, encodes tensor maps
+    torch.cuda.synchronize()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    opt_stream = torch.cuda.Stream()
+    with torch.cuda.graph(g1):
+        job.sync(stream=torch.cuda.current_stream())
+    with torch.cuda.graph(g2):
+        job.overlapped_step(lambda vs: [v.mul_(1.0) for v in vs], opt_stream, stream=torch.cuda.current_stream())
+    for rep, g in enumerate((g1, g2, g1, g2)):
+        src = harness.host_src(ol, 70 + rep)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x3C)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        want = harness.oracle_dst(ol, src, 0x3C)
+        for q, t in job.dst.items():
+            assert np.array_equal(t.cpu().numpy(), want[q]), (rep, q)
+    job.close()
+
+
 @pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8),
                                            ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8)])
 def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
