@@ -28,6 +28,12 @@ class Model:
 
 MODELS = {
     "toy": Model(2, 256, 8, 2, 32, 1024, 512, 1),
+    # edge-case shapes for parity tests: "ragged" (no dimension a multiple of 8:
+    # scalar fallbacks, partial fp8 blocks), "wide" (rows wider than a 32 KiB TMA
+    # stage: column-segmented chunks), "head_only" (no decoder layer)
+    "ragged": Model(1, 20, 5, 5, 4, 30, 10, 1),
+    "wide": Model(1, 64, 2, 1, 32, 20480, 64, 1),
+    "head_only": Model(0, 256, 8, 2, 32, 1024, 512, 1),
     "llama3-8b": Model(32, 4096, 32, 8, 128, 14336, 128256, 1),
     "llama3-70b": Model(80, 8192, 64, 8, 128, 28672, 128256, 1),
     "llama3-405b": Model(126, 16384, 128, 8, 128, 53248, 128256, 1),

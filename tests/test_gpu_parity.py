@@ -144,6 +144,20 @@ def test_toy_parity_pipeline_stages(rt, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("model,fsdp,tpt,tpg,sdt,ddt", [
+    ("ragged", 3, 1, 5, "f32", "bf16"), ("ragged", 7, 5, 1, "bf16", "fp8"), ("ragged", 2, 1, 5, "f32", "f32"),
+    ("ragged", 3, 1, 5, "bf16", "fp8"),
+    ("wide", 2, 2, 1, "f32", "bf16"), ("wide", 3, 1, 2, "bf16", "fp8"), ("wide", 1, 2, 1, "f32", "mxfp8"),
+    ("wide", 2, 2, 1, "bf16", "mxfp4"), ("head_only", 3, 2, 4, "f32", "bf16"), ("toy", 32, 1, 2, "f32", "bf16")])
+def test_edge_shapes_parity(rt, model, fsdp, tpt, tpg, sdt, ddt):
+    """Scalar fallbacks (no dimension a multiple of 8), partial fp8 blocks,
+    rows wider than a TMA stage, a model without decoder layers, and trainer
+    ranks holding nothing (FSDP 32 over 8-row norms)."""
+    job = _toy_job(rt, model, fsdp, tpt, tpg, sdt, ddt)
+    _run_and_compare(rt, job, seed=23)
+    job.close()
+
+
 def test_toy_parity_repeated_syncs(rt):
     """The same plan run many times (epoch counters, no stale state)."""
     job = _toy_job(rt, "toy", 4, 1, 4, "f32", "bf16")

@@ -108,6 +108,36 @@ def test_pipeline_stages_layout_and_plan(L, fsdp, tpt, ppt, tpg, ppg, dp, sdt, d
         assert np.array_equal(got[q], want[q]), q
 
 
+@pytest.mark.parametrize("model,fsdp,tpt,tpg,sdt,ddt", [
+    ("ragged", 3, 1, 5, "f32", "bf16"), ("ragged", 7, 5, 1, "bf16", "fp8"), ("ragged", 2, 1, 5, "f32", "f32"),
+    ("wide", 2, 2, 1, "f32", "bf16"), ("wide", 3, 1, 2, "bf16", "fp8"), ("wide", 1, 2, 1, "f32", "mxfp8"),
+    ("head_only", 3, 2, 4, "f32", "bf16"), ("toy", 32, 1, 2, "f32", "bf16")])   # fsdp 32: empty pieces
+def test_edge_shapes_plan_runs_reproduce_oracle(L, model, fsdp, tpt, tpg, sdt, ddt):
+    m = MODELS[model]
+    S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt)
+    plan = L.Plan(S, D, [0] * S.n_ranks, [0] * D.n_ranks)
+    src, want = brute.build(m, 31, fsdp, tpt, tpg, sdt, ddt)
+    O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt)
+    got_o = [np.zeros(O.dst_rank_bytes(g), np.uint8) for g in range(tpg)]
+    assert O.sync(src, got_o) == 0
+    for a, b in zip(got_o, want):
+        assert np.array_equal(a, b)
+    got = _interpret(L, plan, D, src, sdt, ddt, [w.size for w in want])
+    for g in range(tpg):
+        assert np.array_equal(got[g], want[g]), g
+
+
+def test_mx_rejects_unaligned_shapes(L):
+    """MX formats need whole 1x32 row groups inside every tile (R13, R15)."""
+    S, D = L.describe(MODELS["ragged"], 1, 1, 5, "f32", "mxfp8")
+    with pytest.raises(L.LlrlError) as e:
+        L.Plan(S, D, [0], [0] * 5)
+    assert e.value.status == L.E_UNSUPPORTED
+    with pytest.raises(L.LlrlError) as e:
+        L.describe(MODELS["ragged"], 1, 1, 5, "f32", "mxfp4")
+    assert e.value.status == L.E_UNSUPPORTED
+
+
 def test_layout_errors(L):
     m = MODELS["toy"]
     for args, st in [((1, 1, 3), L.E_INDIVISIBLE), ((1, 1, 16), L.E_INDIVISIBLE), ((1, 3, 2), L.E_INDIVISIBLE),
