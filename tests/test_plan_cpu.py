@@ -279,3 +279,38 @@ def test_plan_bytes_match_baseline_roofline_table(L):
     assert abs(hbm - 35.28) < 0.01 and abs(tx - 5.29) < 0.01
     s = _plan_for(L, "c4", 8).stats()
     assert s.n_fp8_pull_blocks == 0 and s.n_fp8_blocks == 80 * 52224
+
+
+def test_c_abi_error_paths(L):
+    """No exception or abort crosses the ABI: bad arguments come back as status
+    codes with a message (host-only calls; nothing here touches a GPU)."""
+    import ctypes
+    lib = L.lib()
+    m = MODELS["toy"]
+    S, D = L.describe(m, 2, 1, 2)
+    plan = L.Plan(S, D, [0, 1], [0, 1])
+    n = ctypes.c_int64()
+    assert lib.llrl_plan_num_runs(None, ctypes.byref(n)) == L.E_INVALID
+    assert lib.llrl_layout_rank_bytes(S.handle, 99, ctypes.byref(n)) == L.E_INVALID
+    assert b"invalid" in lib.llrl_last_error()
+    v = L.ParamView()
+    assert lib.llrl_layout_param_view(D.handle, 0, 10 ** 6, ctypes.byref(v)) == L.E_INVALID
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    assert lib.llrl_plan_group_range(plan.handle, 2, 0, 0, ctypes.byref(lo), ctypes.byref(hi)) == L.E_INVALID
+    assert lib.llrl_plan_group_range(plan.handle, 0, 0, 99, ctypes.byref(lo), ctypes.byref(hi)) == L.E_INVALID
+    # a two-device plan without a comm: llrl_sync refuses before touching CUDA
+    ptrs = (ctypes.c_void_p * 2)(1 << 20, 1 << 21)
+    assert lib.llrl_sync(plan.handle, None, 0, ptrs, ptrs, None) == L.E_NOPEER
+    assert lib.llrl_sync(plan.handle, None, 7, ptrs, ptrs, None) == L.E_INVALID
+    # device ordinals out of range, mismatched models
+    with pytest.raises(L.LlrlError) as e:
+        L.Plan(S, D, [0, 99], [0, 1])
+    assert e.value.status == L.E_INVALID
+    with pytest.raises(L.LlrlError) as e:
+        L.describe(m, 65, 1, 1)            # more than 64 trainer ranks
+    assert e.value.status == L.E_INVALID
+    # runs: out-of-range requests are errors, in-range ones are exact
+    total = plan.num_runs()
+    assert plan.runs(total - 1, 1).size == 1
+    buf = (L.Run * 2)()
+    assert lib.llrl_plan_get_runs(plan.handle, total - 1, 2, buf) == L.E_INVALID
