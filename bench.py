@@ -135,29 +135,40 @@ def _barrier():
 # ---------------------------------------------------------------- CPU oracle legs
 
 def _oracle_sample(cfg_name, seed=0):
-    """A bounded sample of the workload for the CPU oracle: ONE decoder layer of the
-    config's model (no embed / lm_head), same layout parameters.  Returns
+    """A bounded sample of the workload for the CPU oracle: one decoder layer per
+    pipeline stage of the config's model (no embed / lm_head), same layout parameters.  Returns
     (oracle layout, src buffers, fraction of the full model's elements)."""
     import numpy as np
     import oracle
     from synth import MODELS, CONFIGS
+    import math
     cfg = CONFIGS[cfg_name]
     full = MODELS[cfg.model]
-    m = full.replace(n_layers=1, with_embed=0)
-    ol = oracle.Layout(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner)
-    rng = np.random.default_rng(seed)
+    m = full.replace(n_layers=math.lcm(cfg.pp_train, cfg.pp_gen), with_embed=0)   # whole pipeline stages
+    ol = oracle.Layout(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+    # cheap deterministic values keyed by (param, global row, col): replicated
+    # pieces agree, as the oracle requires (timing sample only)
     src = []
     for r in range(ol.n_src):
-        n = ol.src_rank_bytes(r)
-        if cfg.src_dtype == "f32":
-            src.append((rng.standard_normal(n // 4, dtype=np.float32) * np.float32(0.02)).view(np.uint8))
-        else:
-            x = (rng.standard_normal(n // 2, dtype=np.float32) * np.float32(0.02)).view(np.uint32) >> 16
-            src.append(x.astype(np.uint16).view(np.uint8))
+        buf = np.zeros(ol.src_rank_bytes(r), np.uint8)
+        for p in range(ol.n_src_params):
+            off, r0, r1, c0, c1 = ol.src_piece(r, p)
+            if r1 <= r0 or c1 <= c0:
+                continue
+            rows = np.arange(r0, r1, dtype=np.int64)[:, None]
+            cols = np.arange(c0, c1, dtype=np.int64)[None, :]
+            v = (((rows * 131 + cols * 7 + p * 17 + seed) % 1021) - 510).astype(np.float32) * np.float32(2.0 ** -14)
+            if cfg.src_dtype == "bf16":
+                v = (v.view(np.uint32) >> 16).astype(np.uint16)
+            b = v.view(np.uint8).reshape(-1)
+            buf[off:off + b.size] = b
+        src.append(buf)
     def count(mm):
         L = oracle.Layout(mm, 1, 1, 1)
         return sum(L.src_param_info(p)[0] * L.src_param_info(p)[1] for p in range(L.n_src_params))
     frac = count(m) / count(full)
+    ol.n_layers_sample = m.n_layers
     return ol, src, frac
 
 
@@ -175,7 +186,7 @@ def cpu_baseline(cfg_name, full_model_name):
     ol, src, frac = _oracle_sample(cfg_name)
     dt = _time_oracle_once(ol, src)
     return {"value": round(dt / frac * 1e3, 3), "unit": "ms", "cores": 1, "kind": "oracle",
-            "sample": f"1 decoder layer of {full_model_name} ({frac * 100:.2f}% of the elements), "
+            "sample": f"{ol.n_layers_sample} decoder layer(s) of {full_model_name} ({frac * 100:.2f}% of the elements), "
                       f"oracle/oracle.c single-threaded on {os.cpu_count()} host cores; "
                       f"{dt:.2f} s measured, extrapolated linearly to the whole model"}
 
@@ -192,7 +203,7 @@ def run_reference(args):
         _time_oracle_once(ol, src)
     ts = [_time_oracle_once(ol, src) for _ in range(args.steps)]
     step_ms = sum(ts) / len(ts) / frac * 1e3
-    sample = (f"1 decoder layer of {cfg.model} per step ({frac * 100:.2f}% of the elements), "
+    sample = (f"{ol.n_layers_sample} decoder layer(s) of {cfg.model} per step ({frac * 100:.2f}% of the elements), "
               f"extrapolated linearly to the whole model; oracle/oracle.c single-threaded")
     line = {"impl": "reference", "metric": METRIC, "value": round(step_ms, 3), "unit": "ms",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),

@@ -529,26 +529,28 @@ __global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_
 // HBM over NVLink), releasing a stage once its bulk store has read it.  Data
 // never passes through registers on identity copies (bf16 -> bf16).
 
-constexpr int kCastStageBytes = 32 * 1024;
-constexpr int kCastStages = 4;
-constexpr int kCastWorkers = 512;
+// TMA cast kernel configurations: (stage bytes, stages, worker threads, CTAs/SM)
+#define LLRL_TMA_A 32 * 1024, 4, 512, 1
+#define LLRL_TMA_B 16 * 1024, 4, 256, 2
 
 // Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
 // item, at most kCastStageBytes of source.  Same enumeration on both roles.
 struct Chunk {
     int r0, nr, c0, nc;
 };
+template <int SB>
 __device__ __forceinline__ int cast_chunks(const Item &it, int es, int *rows_per, int *segs_per_row) {
     const int row_bytes = it.cols * es;
-    if (row_bytes <= kCastStageBytes) {
-        *rows_per = kCastStageBytes / row_bytes;
+    if (row_bytes <= SB) {
+        *rows_per = SB / row_bytes;
         *segs_per_row = 1;
         return (it.rows + *rows_per - 1) / *rows_per;
     }
     *rows_per = 1;
-    *segs_per_row = (row_bytes + kCastStageBytes - 1) / kCastStageBytes;
+    *segs_per_row = (row_bytes + SB - 1) / SB;
     return it.rows * *segs_per_row;
 }
+template <int SB>
 __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per, int segs_per_row, int k) {
     Chunk c;
     if (segs_per_row == 1) {
@@ -557,7 +559,7 @@ __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per
         c.c0 = 0;
         c.nc = it.cols;
     } else {
-        const int seg_elems = kCastStageBytes / es;
+        const int seg_elems = SB / es;
         c.r0 = k / segs_per_row;
         c.nr = 1;
         c.c0 = (k % segs_per_row) * seg_elems;
@@ -576,8 +578,9 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <bool SRC_F32>
-__global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __grid_constant__ KParams P) {
+template <bool SRC_F32, int SB, int NST, int NWK, int MINB>
+__global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_constant__ KParams P) {
+    constexpr int kCastStageBytes = SB, kCastStages = NST, kCastWorkers = NWK;
     // warp 0: producer (bulk loads global -> shared), warp 1: storer (bulk stores
     // shared -> global), warps 2..: workers (conversion in shared memory).  A stage
     // moves full (producer -> workers) -> converted (workers -> storer) -> empty
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
         for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
             const Item it = P.items[i];
             int rows_per, segs;
-            const int nch = (it.flags & F_VEC) ? cast_chunks(it, es, &rows_per, &segs) : 1;
+            const int nch = (it.flags & F_VEC) ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
             const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
                     if (lane == 0) mbar_arrive(&full_bar[st]);
                     continue;
                 }
-                const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                 if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
                 __syncwarp();
                 unsigned char *dst = stages + st * kStride;
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
             const Item it = P.items[i];
             int rows_per, segs;
             const bool vec = it.flags & F_VEC;
-            const int nch = vec ? cast_chunks(it, es, &rows_per, &segs) : 1;
+            const int nch = vec ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
             const int des = mx ? 1 : cast ? 2 : es;
@@ -642,7 +645,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
                     continue;
                 }
                 if (lane == 0) {
-                    const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
                     for (int r = 0; r < c.nr; r++) {
                         const int64_t e = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0;   // element offset
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
                 continue;
             }
             int rows_per, segs;
-            const int nch = cast_chunks(it, es, &rows_per, &segs);
+            const int nch = cast_chunks<SB>(it, es, &rows_per, &segs);
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
@@ -701,7 +704,7 @@ __global__ void __launch_bounds__(64 + kCastWorkers, 1) llrl_k_cast_tma(const __
                 unsigned char *in = stages + st * kStride;
                 unsigned char *out = in + kCastStageBytes;
                 if (cast || mx) {
-                    const Chunk c = cast_chunk(it, es, rows_per, segs, k);
+                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                     if (cast) {
                         const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
                         for (int u = wt; u < nunits; u += kCastWorkers) {
@@ -801,13 +804,15 @@ constexpr int kNumCastVariants = int(sizeof(kCastVariants) / sizeof(kCastVariant
 
 static const void *kernel_for(int mode, int variant, bool src_f32) {
     if (mode == 0 && variant == kCastTmaVariant)
-        return src_f32 ? (const void *)llrl_k_cast_tma<true> : (const void *)llrl_k_cast_tma<false>;
+        return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_A> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_A>;
+    if (mode == 0 && variant == kCastTmaVariant + 1)
+        return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_B> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_B>;
     if (mode == 1) {
         if (variant == 0) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
         return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false>;
     }
-    if (variant < 0 || variant >= kNumCastVariants)   // the TMA variant, or out of range
-        return src_f32 ? (const void *)llrl_k_cast_tma<true> : (const void *)llrl_k_cast_tma<false>;
+    if (variant < 0 || variant >= kNumCastVariants)   // out of range: the default TMA variant
+        return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_A> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_A>;
     return src_f32 ? kCastVariants[variant].f32 : kCastVariants[variant].bf16;
 }
 
@@ -816,8 +821,12 @@ static void launch_shape(int mode, int variant, bool src_f32, int *threads, size
     *threads = kThreads;
     *smem = 0;
     if (mode == 0 && variant == kCastTmaVariant) {
-        *threads = 64 + kCastWorkers;
-        *smem = size_t(kCastStages) * (kCastStageBytes + kCastStageBytes / 2);
+        *threads = 64 + 512;
+        *smem = size_t(4) * (32 * 1024 + 16 * 1024);
+    }
+    if (mode == 0 && variant == kCastTmaVariant + 1) {
+        *threads = 64 + 256;
+        *smem = size_t(4) * (16 * 1024 + 8 * 1024);
     }
     if (mode == 1 && variant != 0) {
         *threads = kThreads + 32;
@@ -861,6 +870,6 @@ cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, threads, smem);
 }
 
-int num_cast_variants() { return kNumCastVariants + 1; }   // + the TMA variant
+int num_cast_variants() { return kNumCastVariants + 2; }   // + the two TMA variants
 
 }  // namespace llrl

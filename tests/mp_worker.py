@@ -146,7 +146,7 @@ def main():
     toy_case(runner, world, 3, 1, 2, "bf16", "bf16", "colocated", dp=world // 2 if world >= 4 else 2,
              multicast=True)
     if "--full" in sys.argv:
-        for name in ("c2", "c3", "c4", "c5", "c7"):
+        for name in ("c2", "c3", "c4", "c5", "c7", "c8", "c10"):
             full_case(runner, world, name)
             if dist.get_rank() == 0:
                 print("ok full", name, flush=True)
