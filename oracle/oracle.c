@@ -346,7 +346,7 @@ static int layer_stage(const orc_model *m, int layer, int first_or_last, int pp)
 
 static int src_param_stage(const orc_model *m, int p, int pp)
 {
-    int layer, slot = src_param_slot(m, p, &layer);
+    int layer = -1, slot = src_param_slot(m, p, &layer);
     return layer_stage(m, layer, slot != SLOT_EMBED, pp);
 }
 

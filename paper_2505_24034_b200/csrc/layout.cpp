@@ -236,7 +236,7 @@ llrl_status build_dst(llrl_layout *L) {
         L->rank_bytes[size_t(sg)] = align_up(off);
     }
     // R12: generator DP replicas -- rank d*NS + q is laid out exactly like rank q
-    for (int d = 1; d < L->dp_gen; d++)
+    for (int rep = 1; rep < L->dp_gen; rep++)
         for (int q = 0; q < NS; q++) {
             L->pieces.push_back(L->pieces[size_t(q)]);
             L->rank_bytes.push_back(L->rank_bytes[size_t(q)]);

@@ -553,7 +553,14 @@ llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, con
     P->dev.resize(P->n_devices);
     P->traffic.assign(size_t(P->n_devices) * P->n_devices, 0);
     std::memset(&P->stats, 0, sizeof P->stats);
-    Builder b{src, dst, P, dtype_bytes(src->dtype), dtype_bytes(dst->dtype == LLRL_FP8_E4M3 ? LLRL_BF16 : dst->dtype)};
+    // es_dst: element size of NON-quantised generator tensors (quantised formats keep
+    // embed / lm_head / norms in bf16, R7 / R13 / R15)
+    Builder b{};
+    b.S = src;
+    b.D = dst;
+    b.P = P;
+    b.es_src = dtype_bytes(src->dtype);
+    b.es_dst = dtype_bytes(dst->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
     llrl_status st = b.make_tiles();
     if (st == LLRL_OK) st = b.make_items();
     if (st != LLRL_OK) { delete P; return st; }

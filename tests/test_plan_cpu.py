@@ -314,3 +314,33 @@ def test_c_abi_error_paths(L):
     assert plan.runs(total - 1, 1).size == 1
     buf = (L.Run * 2)()
     assert lib.llrl_plan_get_runs(plan.handle, total - 1, 2, buf) == L.E_INVALID
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_plan_algorithmic_bytes_equal_layout_bytes(L, name):
+    """The roofline's algorithmic bytes: every byte of every trainer piece is read
+    once per generator rank it feeds and every generator byte (data + scales) is
+    written once -- checked against the layouts for every benchmark config
+    (2-layer versions of the big models)."""
+    cfg = CONFIGS[name]
+    m = MODELS[cfg.model]
+    m = m.replace(n_layers=max(2, cfg.pp_train, cfg.pp_gen)) if m.n_layers > 2 else m
+    S, D = L.describe(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                      cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+    sd, dd = placement(cfg, 4)
+    plan = L.Plan(S, D, sd, dd)
+    st = plan.stats()
+    want_dst = 0
+    for g in range(D.n_ranks):
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            n = v.rows * v.cols
+            if v.quantised:
+                data = n // 2 if cfg.dst_dtype == "mxfp4" else n
+                scales = -(-v.rows // 128) * -(-v.cols // 128) * 4 if cfg.dst_dtype == "fp8" else v.rows * -(-v.cols // 32)
+                want_dst += data + scales
+            else:
+                want_dst += n * {"f32": 4}.get(cfg.dst_dtype, 2)
+    assert st.dst_bytes == want_dst
+    dev = [plan.device_bytes(d) for d in range(st.n_devices)]
+    assert sum(b["hbm_write"] for b in dev) == st.dst_bytes and sum(b["hbm_read"] for b in dev) == st.src_bytes
