@@ -398,3 +398,13 @@ def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
         for g in job.dst:
             assert np.array_equal(hd[g].numpy(), want[g]), (rep, g)
     job.close()
+
+
+@pytest.mark.parametrize("max_ctas", [1, 3, 64])
+def test_toy_parity_capped_grid(rt, max_ctas):
+    """llrl_plan_set_max_ctas: a capped grid (down to one CTA) still covers every item."""
+    for sdt, ddt in (("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp4")):
+        job = _toy_job(rt, "toy", 3, 2, 4, sdt, ddt)
+        job.plan.set_max_ctas(job.device, max_ctas)
+        _run_and_compare(rt, job, seed=max_ctas)
+        job.close()
