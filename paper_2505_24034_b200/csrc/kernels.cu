@@ -641,7 +641,16 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 const int st = n % kCastStages;
                 mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
                 if (!vec) {                       // scalar item: workers wrote global memory directly
-                    if (lane == 0) mbar_arrive(&empty_bar[st]);
+                    if (lane == 0) {
+                        // release the deferred stage now: the producer may need it before
+                        // another vector chunk arrives (deadlock with few CTAs otherwise)
+                        if (pend >= 0) {
+                            bulk_wait_read<0>();
+                            mbar_arrive(&empty_bar[pend]);
+                            pend = -1;
+                        }
+                        mbar_arrive(&empty_bar[st]);
+                    }
                     continue;
                 }
                 if (lane == 0) {
