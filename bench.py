@@ -64,7 +64,7 @@ class ClockSampler:
                     self.samples.append(f)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -306,11 +306,11 @@ def run_llrl(args):
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "ms_min": round(ms_min, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": "synthetic (counter-based Llama-init-scale weights)",
-            "config": {"workload": _workload_name(cfg, args.gpus), "model": cfg.model,
+            "config": {"workload": _workload_name(cfg, args.gpus), "shapes": cfg.model,
                        "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
                        "max_ctas": args.max_ctas or "all SMs",
                        "multicast": bool(args.multicast and job.mc_positions()[0]),
-                       "layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
+                       "n_layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
                        "l2": "inputs >> 126 MB L2 (no flush needed)"},
             "throughput": {"gen_bytes_per_s_GB": round(tot.dst_bytes / (ms * 1e6), 1),
