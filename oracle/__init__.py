@@ -19,7 +19,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED = 0, -1, -2, -3, -4
 E_NOMEM, E_UNCOVERED, E_OVERLAP = -7, -8, -9
-DTYPES = {"f32": 0, "bf16": 1, "fp8": 2, "mxfp8": 3, "mxfp4": 4}
+DTYPES = {"f32": 0, "bf16": 1, "fp8": 2, "mxfp8": 3, "mxfp4": 4, "nvfp4": 5}
 
 
 def build(force: bool = False) -> str:
@@ -62,6 +62,11 @@ def lib():
         L.orc_mx_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_mx4_block.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_e2m1_array.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_nv_tensor_scales.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.orc_nv_tensor_scales.restype = ctypes.c_float
+        L.orc_nv_group.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_dst_tensor_scale_off.argtypes = [M, C, ctypes.c_int, ctypes.c_int]
+        L.orc_dst_tensor_scale_off.restype = ctypes.c_int64
         L.orc_num_src_params.argtypes, L.orc_num_src_params.restype = [M], ctypes.c_int
         L.orc_num_dst_params.argtypes, L.orc_num_dst_params.restype = [M], ctypes.c_int
         L.orc_src_param_info.argtypes = [M, ctypes.c_int, i64p, i64p, ip]
@@ -130,6 +135,23 @@ def mx4_block(x: np.ndarray):
     return q, int(s[0])
 
 
+def nv_tensor_scales(x: np.ndarray):
+    """NVFP4 per-tensor scales -> (S_dec, S_enc)."""
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1)
+    enc = ctypes.c_float()
+    dec = lib().orc_nv_tensor_scales(_ptr(x), x.size, ctypes.byref(enc))
+    return np.float32(dec), np.float32(enc.value)
+
+
+def nv_group(x: np.ndarray, s_enc):
+    """One NVFP4 group (<= 16 elements) -> (codes one per element, E4M3 scale byte)."""
+    x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1)
+    q = np.empty(x.shape, dtype=np.uint8)
+    s = np.zeros(1, dtype=np.uint8)
+    lib().orc_nv_group(_ptr(x), x.size, float(s_enc), _ptr(q), _ptr(s))
+    return q, int(s[0])
+
+
 class Layout:
     """The oracle's own view of both layouts for one configuration."""
 
@@ -171,6 +193,9 @@ class Layout:
                                  ctypes.byref(C), ctypes.byref(q), ctypes.byref(o), ctypes.byref(s))
         assert rc == 0
         return R.value, C.value, q.value, o.value, s.value
+
+    def dst_tensor_scale_off(self, g, gp):
+        return lib().orc_dst_tensor_scale_off(ctypes.byref(self.m), ctypes.byref(self.c), g, gp)
 
     def dst_element_source(self, g, gp, lr, lc):
         p, r, c = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()

@@ -45,7 +45,7 @@
 #define ORC_E_OVERLAP -9      /* a generator byte would be written twice */
 #define ORC_E_NOMEM -7
 
-enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2, ORC_MXFP8 = 3, ORC_MXFP4 = 4 };
+enum { ORC_F32 = 0, ORC_BF16 = 1, ORC_FP8 = 2, ORC_MXFP8 = 3, ORC_MXFP4 = 4, ORC_NVFP4 = 5 };
 
 typedef struct {
     int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, with_embed;
@@ -206,6 +206,53 @@ void orc_mx4_block(const float *x, int64_t n, uint8_t *q, uint8_t *scale)
         q[i] = e2m1_encode(fabs(ldexp((double)x[i], -X)), (uint8_t)((vb >> 31) << 3));
     }
     *scale = (uint8_t)(X + 127);
+}
+
+/* E4M3FN code -> its exact value (used to decode NVFP4 block scales). */
+static double e4m3_decode(uint8_t code)
+{
+    int sign = code >> 7, E = (code >> 3) & 0xF, m = code & 0x7;
+    double v = E == 0 ? ldexp((double)m, -9) : ldexp(1.0 + m / 8.0, E - 7);
+    return sign ? -v : v;
+}
+
+/* NVFP4 (reading R16): E2M1 elements in 1x16 row groups with an E4M3 scale per
+ * group and one fp32 scale per generator tensor.  Per tensor: amax_t over the
+ * whole generator-local tensor, A = max(amax_t, 2^-64), S_enc = 2688 / A,
+ * S_dec = A / 2688 (fp32 RN; 2688 = 448 * 6).  Per group: s = (amax_g / 6) *
+ * S_enc (two fp32 RN operations), its E4M3 code sb = e4m3_rn_satfinite(s) and
+ * decoded value s_q; r = S_enc / s_q (fp32 RN; r = 0 when s_q = 0); element
+ * q = e2m1_rn_satfinite(x * r) (fp32 RN product).  Stored: packed codes, the
+ * group scale codes, S_dec. */
+float orc_nv_tensor_scales(const float *x, int64_t n, float *s_enc)
+{
+    float amax = 0.0f;
+    for (int64_t i = 0; i < n; i++)
+        if (fabsf(x[i]) > amax)
+            amax = fabsf(x[i]);
+    const float A = amax > 0x1p-64f ? amax : 0x1p-64f;
+    volatile float enc = 2688.0f / A;
+    volatile float dec = A / 2688.0f;
+    *s_enc = enc;
+    return dec;
+}
+
+void orc_nv_group(const float *x, int64_t n, float s_enc, uint8_t *q, uint8_t *scale)
+{
+    float amax = 0.0f;
+    for (int64_t i = 0; i < n; i++)
+        if (fabsf(x[i]) > amax)
+            amax = fabsf(x[i]);
+    volatile float t = amax / 6.0f;
+    volatile float sv = t * s_enc;
+    const uint8_t code = orc_e4m3_rn_satfinite(sv);
+    const float sq = (float)e4m3_decode(code);     /* exact: e4m3 values are fp32-representable */
+    volatile float r = sq == 0.0f ? 0.0f : s_enc / sq;
+    for (int64_t i = 0; i < n; i++) {
+        volatile float y = x[i] * r;
+        q[i] = orc_e2m1_rn_satfinite(y);
+    }
+    *scale = code;
 }
 
 /* One MXFP8 block (OCP Microscaling Formats v1.0, E4M3 elements; DESIGN.md
@@ -379,12 +426,15 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (c->dst_dtype == ORC_MXFP4 && (m->d_model % 32 || (m->n_heads * m->head_dim / c->tp_gen) % 32 ||
                                       (m->d_ffn / c->tp_gen) % 32))
         return ORC_E_UNSUPPORTED;
+    if (c->dst_dtype == ORC_NVFP4 && (m->d_model % 16 || (m->n_heads * m->head_dim / c->tp_gen) % 16 ||
+                                      (m->d_ffn / c->tp_gen) % 16))
+        return ORC_E_UNSUPPORTED;
     /* R14: whole layers per stage */
     if (m->n_layers % c->pp_train || m->n_layers % c->pp_gen)
         return ORC_E_INDIVISIBLE;
     if (c->src_dtype != ORC_F32 && c->src_dtype != ORC_BF16)
         return ORC_E_UNSUPPORTED;
-    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_MXFP4)
+    if (c->dst_dtype < ORC_F32 || c->dst_dtype > ORC_NVFP4)
         return ORC_E_UNSUPPORTED;
     if (c->dst_dtype == ORC_F32 && c->src_dtype != ORC_F32)
         return ORC_E_UNSUPPORTED;
@@ -561,7 +611,8 @@ static int dst_parts(const orc_model *m, const orc_cfg *c, int g, int stage, int
     default:
         return -1;
     }
-    if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8 && c->dst_dtype != ORC_MXFP4)
+    if (c->dst_dtype != ORC_FP8 && c->dst_dtype != ORC_MXFP8 && c->dst_dtype != ORC_MXFP4 &&
+        c->dst_dtype != ORC_NVFP4)
         *quant = 0;
     if (stage >= 0 && layer_stage(m, layer, gs != G_EMBED, c->pp_gen) != stage) {
         *rows = 0; *cols = 0;          /* R14: not on this generator stage */
@@ -577,7 +628,7 @@ static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int64_t data_bytes(const orc_cfg *c, int64_t R, int64_t C, int qt)
 {
     if (qt)
-        return c->dst_dtype == ORC_MXFP4 ? R * C / 2 : R * C;
+        return (c->dst_dtype == ORC_MXFP4 || c->dst_dtype == ORC_NVFP4) ? R * C / 2 : R * C;
     return R * C * (c->dst_dtype == ORC_F32 ? 4 : 2);
 }
 
@@ -587,6 +638,8 @@ static int64_t scale_grid_bytes(const orc_cfg *c, int64_t R, int64_t C)
 {
     if (c->dst_dtype == ORC_MXFP8 || c->dst_dtype == ORC_MXFP4)
         return R * cdiv(C, 32);
+    if (c->dst_dtype == ORC_NVFP4)
+        return R * cdiv(C, 16);
     return cdiv(R, 128) * cdiv(C, 128) * 4;
 }
 
@@ -614,6 +667,10 @@ int orc_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
             off = align256(off);
             s_off = off;
             off += scale_grid_bytes(c, R, C);
+            if (c->dst_dtype == ORC_NVFP4) {   /* R16: fp32 tensor scale at the next 256-byte boundary */
+                off = align256(off);
+                off += 4;
+            }
         }
         if (q == gp) {
             *rows = R; *cols = C; *quant = qt; *byte_off = data_off; *scale_off = s_off;
@@ -633,7 +690,18 @@ int64_t orc_dst_rank_bytes(const orc_model *m, const orc_cfg *c, int g)
     int64_t end = off + data_bytes(c, R, C, qt);
     if (qt)
         end = soff + scale_grid_bytes(c, R, C);
+    if (qt && c->dst_dtype == ORC_NVFP4)
+        end = align256(end) + 4;
     return align256(end);
+}
+
+/* R16: byte offset of an NVFP4 tensor's fp32 scale (-1 if none). */
+int64_t orc_dst_tensor_scale_off(const orc_model *m, const orc_cfg *c, int g, int gp)
+{
+    int64_t R, C, off, soff; int qt;
+    if (orc_dst_param(m, c, g, gp, &R, &C, &qt, &off, &soff) || !qt || c->dst_dtype != ORC_NVFP4)
+        return -1;
+    return align256(soff + scale_grid_bytes(c, R, C));
 }
 
 /* For point checks at full size: generator element (g, gp, lr, lc) comes
@@ -745,7 +813,24 @@ static int write_dst_param(const orc_model *m, const orc_cfg *c, int g, int gp,
     }
     /* Step 3-4: cast and store */
     int rc = ORC_OK;
-    if (qt && c->dst_dtype == ORC_MXFP4) {
+    if (qt && c->dst_dtype == ORC_NVFP4) {
+        int64_t nsc = cdiv(C, 16);
+        int64_t ts = align256(soff + R * nsc);
+        if ((rc = mark_written(written, off, R * C / 2)) || (rc = mark_written(written, soff, R * nsc)) ||
+            (rc = mark_written(written, ts, 4)))
+            goto out;
+        float s_enc;
+        float s_dec = orc_nv_tensor_scales(local, R * C, &s_enc);
+        memcpy(dst + ts, &s_dec, 4);
+        uint8_t codes[16];
+        for (int64_t r = 0; r < R; r++)
+            for (int64_t j = 0; j < nsc; j++) {
+                int64_t n = C - j * 16 < 16 ? C - j * 16 : 16;
+                orc_nv_group(local + r * C + j * 16, n, s_enc, codes, dst + soff + r * nsc + j);
+                for (int64_t k = 0; k < n; k += 2)   /* even element -> low nibble */
+                    dst[off + (r * C + j * 16 + k) / 2] = (uint8_t)(codes[k] | (codes[k + 1] << 4));
+            }
+    } else if (qt && c->dst_dtype == ORC_MXFP4) {
         int64_t nsc = cdiv(C, 32);
         if ((rc = mark_written(written, off, R * C / 2)) || (rc = mark_written(written, soff, R * nsc)))
             goto out;

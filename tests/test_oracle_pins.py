@@ -198,6 +198,39 @@ def test_mx4_block_vs_numpy_ml_dtypes(oracle_lib, kind):
         assert np.array_equal((qq[0::2] | (qq[1::2] << 4)).astype(np.uint8), packed[r])
 
 
+@pytest.mark.parametrize("kind", ["random", "zero_groups", "outlier", "tiny", "wide_range", "partial"])
+def test_nvfp4_vs_numpy_ml_dtypes(oracle_lib, kind):
+    """NVFP4 (R16): per-tensor and per-group scales vs numpy fp32 + ml_dtypes;
+    'outlier' drives most group scales into E4M3 subnormals, 'zero_groups' the
+    s_q = 0 branch, 'tiny' the 2^-64 amax floor."""
+    rng = np.random.default_rng(13)
+    R, C = 16, 64
+    x = rng.normal(0, 0.02, (R, C)).astype(np.float32)
+    if kind == "zero_groups":
+        x[:, 16:32] = 0
+        x[3] = 0
+    elif kind == "outlier":
+        x[5, 7] = 1e4
+    elif kind == "tiny":
+        x = (x * 1e-30).astype(np.float32)
+    elif kind == "wide_range":
+        x = (x * 10.0 ** rng.uniform(-20, 20, (R, 1))).astype(np.float32)
+    elif kind == "partial":
+        x = x[:, :40]
+        C = 40
+    packed, sb, ts = brute.nv_quant(x)
+    dec, enc = oracle.nv_tensor_scales(x)
+    assert dec == ts[0]
+    for r in range(R):
+        for j in range(-(-C // 16)):
+            q, sc = oracle.nv_group(x[r, j * 16:(j + 1) * 16], enc)
+            assert sc == sb[r, j], (r, j)
+            qq = np.zeros(len(q) + (len(q) & 1), np.uint8)
+            qq[:len(q)] = q
+            assert np.array_equal((qq[0::2] | (qq[1::2] << 4)).astype(np.uint8),
+                                  packed[r, j * 8:j * 8 + len(qq) // 2]), (r, j)
+
+
 # --------------------------------------------------------------------------- layout / sync
 
 def _run_oracle(m, fsdp, tpt, tpg, sdt, ddt, inner, src, sentinel=0):
@@ -240,6 +273,8 @@ def test_oracle_vs_brute_toy_sweep_bf16(oracle_lib, fsdp, tpt, tpg):
     (1, 8, 8, "bf16", "mxfp8", False),
     (3, 1, 4, "f32", "mxfp4", False),     # MXFP4 (R15)
     (2, 2, 8, "bf16", "mxfp4", True),
+    (2, 1, 2, "f32", "nvfp4", False),     # NVFP4 (R16)
+    (2, 2, 8, "bf16", "nvfp4", True),
 ])
 def test_oracle_vs_brute_odd_layouts(oracle_lib, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]
