@@ -56,7 +56,12 @@ typedef enum {
  * reading R13); scale grid [R, ceil(C/32)] bytes after each quantised weight. */
 /* LLRL_MXFP4: OCP MX E2M1 elements (two per byte, even element in the low
  * nibble) with one E8M0 scale byte per 1x32 row group (reading R15). */
-typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3, LLRL_MXFP4 = 4 } llrl_dtype;
+/* LLRL_NVFP4: E2M1 elements (packed like MXFP4) with one E4M3 scale per 1x16
+ * row group and one fp32 scale per generator tensor (reading R16); the tensor
+ * scale needs the tensor's global amax, a cross-GPU max-reduction inside the
+ * sync (llrl_sync only; llrl_sync_group / llrl_sync_host return UNSUPPORTED). */
+typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3, LLRL_MXFP4 = 4,
+               LLRL_NVFP4 = 5 } llrl_dtype;
 
 /* Llama-style decoder shapes (Llama-3.1 config.json fields [ext]). */
 typedef struct {
@@ -89,13 +94,15 @@ typedef struct {
     int64_t full_r0, full_c0;  /* src side: top-left of the piece in the full tensor; dst: 0 */
     int32_t src_param;   /* src side: canonical source-param id; dst side: -1 */
     int32_t is_norm;
+    int64_t tensor_scale_off;  /* NVFP4: byte offset of the fp32 tensor scale, else -1 */
 } llrl_param_view;
 
 /* ---- a1: layouts ------------------------------------------------------------
  * Describe the trainer (src) and generator (dst) layouts of `m` for a trainer
  * mesh fsdp x tp_train (fsdp*tp_train ranks, R1-R3) and a generator with
  * tp_gen ranks (R4).  src_dtype in {F32, BF16}; dst_dtype in {F32 (only from
- * F32: identity/provenance mode), BF16, FP8_E4M3 (R7), MXFP8 (R13), MXFP4 (R15)}.
+ * F32: identity/provenance mode), BF16, FP8_E4M3 (R7), MXFP8 (R13), MXFP4 (R15),
+ * NVFP4 (R16)}.
  * Errors: INVALID (NULL, non-positive sizes), INDIVISIBLE, UNSUPPORTED.
  * Ownership: *src_out and *dst_out belong to the caller (llrl_layout_destroy). */
 llrl_status llrl_layout_describe(const llrl_model *m, int fsdp, int tp_train, int tp_gen,
@@ -179,10 +186,10 @@ typedef struct {
 llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
 
 /* ---- completion comm (a6) --------------------------------------------------
- * A comm owns one 1 KiB flag buffer on `device`: word s counts data arrivals
- * from sender device s, word 16 + s counts "trainer bytes staged"
- * announcements of device s (llrl_sync_host with pull items), word 32 is set
- * if a wait timed out (30 s), words 64.. hold the arrivals expected so far.
+ * A comm owns one 1 MiB buffer on `device`: per-sender-device counters of data
+ * arrivals, "trainer bytes staged" announcements (llrl_sync_host with pull
+ * items) and the NVFP4 amax / scale handshake, a timeout flag (a wait gave up
+ * after 30 s), the arrivals expected so far, and the NVFP4 amax table.
  * All counters are cumulative and live on the device: llrl_sync /
  * llrl_sync_group launch identical parameters on every call, so after one
  * warm-up call they can be captured in a CUDA graph and replayed.

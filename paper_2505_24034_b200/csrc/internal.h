@@ -18,6 +18,7 @@ constexpr int kMaxDevices = 16;
 constexpr int64_t kAlign = 256;    // R0: every piece starts at a 256-byte boundary
 constexpr int kFp8Block = 128;     // R7
 constexpr int kMxGroup = 32;       // R13
+constexpr int kNvGroup = 16;       // R16
 
 void set_error(const char *fmt, ...);
 int64_t dtype_bytes(int dt);
@@ -61,6 +62,7 @@ struct Piece {          // one parameter on one rank
     int64_t rows, cols; // local shape
     int64_t byte_off;
     int64_t scale_off = -1;
+    int64_t tscale_off = -1;      // NVFP4 fp32 tensor scale (R16)
     bool quantised = false;
     int dtype;
     std::vector<DstPart> parts;   // dst side only
@@ -95,17 +97,18 @@ std::vector<SrcParam> enumerate_src_params(const llrl_model &m);
 
 namespace llrl {
 
-enum ItemKind : uint16_t {
+enum ItemKind : uint8_t {
     K_CAST = 0,        // 2-D (or 1-D when rows == 1) relayout + cast to bf16 / copy to f32
     K_FP8 = 1,         // one 128x128 (or edge) fp8 block, single source
     K_FP8_MULTI = 2,   // one fp8 block gathered from several sources (pull, R8)
 };
-enum ItemFlag : uint16_t {
+enum ItemFlag : uint8_t {
     F_VEC = 1,         // 16-byte vector path legal (offsets / lds / cols aligned)
     F_DST_F32 = 2,     // destination dtype f32 (identity), else bf16 (K_CAST)
     F_MX = 4,          // K_CAST into MXFP8 codes (1 byte); aux = scale byte base (R13)
     F_MC = 8,          // K_CAST stored through the NVLS multicast VA of dst_rank's position (f1)
     F_FP4 = 16,        // with F_MX: MXFP4 (E2M1 codes, two per byte; dst offsets in 4-bit elements) (R15)
+    F_NV = 32,         // with F_MX | F_FP4: NVFP4 1x16 groups, E4M3 group scales, per-tensor scale (R16)
 };
 
 // Device work item (48 bytes).  Offsets in elements of each side's dtype, except
@@ -118,8 +121,9 @@ struct alignas(16) Item {
     int64_t aux;
     int32_t rows, cols;
     int32_t src_ld, dst_ld;
-    uint16_t src_rank, dst_rank;
-    uint16_t kind, flags;
+    uint8_t src_rank, dst_rank;   // < kMaxRanks (K_FP8_MULTI: src_rank = segment count)
+    uint8_t kind, flags;
+    int32_t tid;                  // NVFP4 (F_NV): generator tensor id (amax table row), else -1
 };
 static_assert(sizeof(Item) == 48, "Item layout");
 
@@ -160,6 +164,17 @@ struct DeviceWork {
     std::vector<Seg> segs;
     std::vector<TmaRef> tma_refs;      // one per fp8 item (index i - n_cast)
     std::vector<void *> dst_mc;        // multicast VA per dst rank (llrl_plan_set_multicast)
+    // NVFP4 (R16) per-tensor amax handshake
+    std::vector<int32_t> nv_contrib;   // tensor ids this device's items quantise
+    std::vector<int> nv_targets;       // devices holding those tensors (amax -> them, ready <- them)
+    std::vector<int32_t> nv_local;     // tensor ids held by this device
+    std::vector<int> nv_senders;       // devices contributing to them
+    uint32_t *d_nv_partial = nullptr;  // [n_tensors] local partial amax (u32 bits)
+    uint32_t *d_nv_amax = nullptr;     // [n_tensors] global amax fetched for the quantiser
+    int32_t *d_nv_contrib = nullptr, *d_nv_tensor_dev = nullptr;
+    struct NvLocal { int32_t tid, dst_rank; int64_t tscale_off; };
+    NvLocal *d_nv_local = nullptr;
+    unsigned long long *d_nv_done = nullptr;
     std::vector<char> src_touched, dst_touched;   // ranks this device's items read / write
     bool touched_valid = false;
     bool has_mc = false;
@@ -200,6 +215,9 @@ struct DeviceWork {
 struct llrl_plan {
     int n_src, n_dst, n_devices;
     bool multicast = false;
+    bool nv = false;                     // NVFP4 destination (R16)
+    struct NvTensor { int32_t dst_rank, dst_param, device; int64_t tscale_off; };
+    std::vector<NvTensor> nv_tensors;    // tensor id -> generator tensor
     int src_dtype, dst_dtype;
     std::vector<int> src_device, dst_device;
     std::vector<int64_t> src_rank_bytes, dst_rank_bytes;
@@ -214,10 +232,8 @@ struct llrl_plan {
 
 struct llrl_comm {
     int device;
-    // flags[s]: data arrivals from sender device s; flags[kMaxDevices + s]:
-    // "trainer bytes staged" announcements from device s (llrl_sync_host);
-    // flags[2 * kMaxDevices]: wait-timeout flag; flags[4 * kMaxDevices + slot]:
-    // arrivals expected so far (device-side, local).  1 KiB.
+    // 1 MiB device buffer: completion counters, expected counts and the NVFP4
+    // amax table; layout in kernels.h (kSlot*, kFlag*, kNvTableOffset).
     unsigned long long *flags = nullptr;
     unsigned long long *peer_flags[llrl::kMaxDevices] = {};
     bool ipc_opened[llrl::kMaxDevices] = {};

@@ -232,6 +232,13 @@ __device__ __forceinline__ uint4 quant16(const uint4 *w, float inv) {
     return make_uint4(ow[0], ow[1], ow[2], ow[3]);
 }
 
+// Exact value of an E4M3FN code (finite codes only).
+__device__ __forceinline__ float e4m3_value(uint32_t code) {
+    const uint32_t E = (code >> 3) & 0xF, m = code & 0x7;
+    const float v = E == 0 ? float(m) * 0x1p-9f : __uint_as_float(((E + 120u) << 23) | (m << 20));
+    return (code & 0x80) ? -v : v;
+}
+
 // 16 source elements (W words) -> 16 e2m1 codes, two per byte, the even
 // element in the low nibble (cvt.e2m1x2 puts its first operand in the high nibble).
 template <bool SRC_F32, int W>
@@ -723,7 +730,14 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                            bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
                         }
                     } else {
-                        // MX (R13 / R15): lanes (2j, 2j+1) hold the two halves of one 1x32 group
+                        const bool nv = it.flags & F_NV;
+                        float s_enc = 0.0f;
+                        if (nv) {   // R16: S_enc = 2688 / max(A, 2^-64) from the tensor's global amax
+                            const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
+                            s_enc = __fdiv_rn(2688.0f, A);
+                        }
+                        // MX (R13 / R15): lanes (2j, 2j+1) hold the two halves of one 1x32 group;
+                        // NVFP4 (R16): each thread's 16 elements are one 1x16 group
                         const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
                         for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
                             const int u = u0 + wt;
@@ -735,6 +749,20 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             for (int j = 0; j < W; j++) {
                                 w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
                                 amax = word_amax<SRC_F32>(w[j], amax);
+                            }
+                            if (nv) {
+                                // group scale s = (amax / 6) * S_enc -> E4M3 code; r = S_enc / s_q
+                                const float t6 = __fdiv_rn(__uint_as_float(amax), 6.0f);
+                                const uint32_t sc = e4m3x2_rn(__fmul_rn(t6, s_enc), 0.0f) & 0xFFu;
+                                const float sq = e4m3_value(sc);
+                                const float r = sq == 0.0f ? 0.0f : __fdiv_rn(s_enc, sq);
+                                if (live) {
+                                    reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, r);
+                                    const int e0 = u * 16, rr = e0 / c.nc, cc = e0 - rr * c.nc;
+                                    const int64_t o = it.dst_off + int64_t(c.r0 + rr) * it.dst_ld + c.c0 + cc;
+                                    dbase[it.aux + o / kNvGroup] = static_cast<char>(sc);
+                                }
+                                continue;
                             }
                             amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
                             // shared exponent floor(log2 amax) - emax (8 for E4M3, 2 for E2M1),
@@ -762,15 +790,96 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
     complete(P);
 }
 
-// K3 receiver: lane s spins (acquire, system scope) until flag slot s reaches
-// its target (0 = not waited on): slots 0..15 count data arrivals per sender
-// device, 16..31 "trainer bytes staged" announcements per device.  One counter
+// ---- NVFP4 (R16) per-tensor amax: a max-reduction across the GPUs that feed
+// each generator tensor, run inside the sync before the quantisation.
+// Phase A (llrl_k_nv_amax, every contributing GPU): block max |x| of every
+// NVFP4 item -> atomicMax into a local partial per tensor; the last CTA
+// writes each partial into row [tensor][my device] of the owning GPU's table
+// and signals it.  Phase B (llrl_k_nv_scale, owning GPU, after all partials
+// arrived): global amax = max of the row, kept in the row's last word; the
+// fp32 tensor scale A / 2688 goes into the generator buffer; partial words are
+// cleared for the next sync; contributors are signalled.  Phase C
+// (llrl_k_nv_fetch, contributors): copy the global amax of each contributed
+// tensor into a local array the quantising kernel reads.
+template <bool SRC_F32>
+__global__ void __launch_bounds__(kThreads) llrl_k_nv_amax(const __grid_constant__ NvAmaxParams P) {
+    __shared__ uint32_t s_red[2][kThreads / 32];
+    constexpr int es = SRC_F32 ? 4 : 2;
+    int k = 0;
+    for (int i = blockIdx.x; i < P.n_items; i += gridDim.x) {
+        const Item it = P.items[i];
+        if (!(it.flags & F_NV)) continue;
+        const char *src = static_cast<const char *>(P.src[it.src_rank]);
+        uint32_t amax = 0;
+        const int vpr = it.cols * es / 16;               // 16-byte words per row (cols % 16 == 0)
+        for (int v = threadIdx.x; v < it.rows * vpr; v += kThreads) {
+            const int r = v / vpr, c = v - r * vpr;
+            amax = word_amax<SRC_F32>(ld_stream(src + (it.src_off + int64_t(r) * it.src_ld) * es + c * 16), amax);
+        }
+        amax = block_max_u32(amax, s_red[k & 1]);
+        if (threadIdx.x == 0) atomicMax(P.partial + it.tid, amax);
+        k++;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        const unsigned long long prev = atomicAdd(P.done, 1ULL);
+        last = prev + 1 == gridDim.x;
+        if (last) atomicExch(P.done, 0ULL);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int j = threadIdx.x; j < P.n_contrib; j += kThreads) {
+        const int tid = P.contrib[j];
+        const uint32_t v = atomicAdd(P.partial + tid, 0u);      // coherent read of the partial
+        P.tables[P.tensor_dev[tid]][tid * kNvTableStride + P.my_dev] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < P.n_signal; s++)
+            asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(P.signal[s]) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) llrl_k_nv_scale(const __grid_constant__ NvScaleParams P) {
+    const auto *loc = static_cast<const DeviceWork::NvLocal *>(P.locals);
+    for (int j = threadIdx.x; j < P.n_local; j += kThreads) {
+        uint32_t *row = P.table + loc[j].tid * kNvTableStride;
+        uint32_t a = 0;
+        for (int s = 0; s < kMaxDevices; s++) {
+            a = max(a, row[s]);
+            row[s] = 0;                                   // ready for the next sync
+        }
+        row[kMaxDevices] = a;
+        const float A = fmaxf(__uint_as_float(a), 0x1p-64f);
+        *reinterpret_cast<float *>(static_cast<char *>(P.dst[loc[j].dst_rank]) + loc[j].tscale_off) =
+            __fdiv_rn(A, 2688.0f);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < P.n_signal; s++)
+            asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(P.signal[s]) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) llrl_k_nv_fetch(const __grid_constant__ NvFetchParams P) {
+    for (int j = threadIdx.x; j < P.n_contrib; j += kThreads) {
+        const int tid = P.contrib[j];
+        P.amax_out[tid] = P.tables[P.tensor_dev[tid]][tid * kNvTableStride + kMaxDevices];
+    }
+}
+
+// K3 receiver: thread s spins (acquire, system scope) until flag slot s reaches
+// its target (0 = not waited on): slot ranges as in kernels.h (data arrivals,
+// staging announcements, NVFP4 amax / ready per device).  One counter
 // per sender, so a fast sender's later arrivals can never stand in for a slow
 // sender's.  Bounded by a timeout so a missing peer cannot hang the GPU; on
 // timeout flag[2 * kMaxDevices] = 1.
 __global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned long long timeout_ns) {
     const int s = threadIdx.x;
-    if (s >= 2 * kMaxDevices || t.count[s] == 0) return;
+    if (s >= kNumSlots || t.count[s] == 0) return;
     // expected arrivals live on the device (flags[kExpected + s]): graph-replayable
     unsigned long long *expected = flags + kFlagExpected + s;
     const unsigned long long target = *expected + t.count[s];
@@ -782,7 +891,7 @@ __global__ void llrl_k_wait(unsigned long long *flags, WaitTargets t, unsigned l
         if (v >= target) return;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         if (now - t0 > timeout_ns) {
-            atomicExch(flags + 2 * kMaxDevices, 1ULL);
+            atomicExch(flags + kFlagTimeout, 1ULL);
             return;
         }
         __nanosleep(256);
@@ -858,13 +967,29 @@ cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, i
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
 }
 
+cudaError_t launch_nv_amax(const NvAmaxParams &P, bool src_f32, int grid, cudaStream_t stream) {
+    if (src_f32) llrl_k_nv_amax<true><<<grid, kThreads, 0, stream>>>(P);
+    else llrl_k_nv_amax<false><<<grid, kThreads, 0, stream>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nv_scale(const NvScaleParams &P, cudaStream_t stream) {
+    llrl_k_nv_scale<<<1, kThreads, 0, stream>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nv_fetch(const NvFetchParams &P, cudaStream_t stream) {
+    llrl_k_nv_fetch<<<1, kThreads, 0, stream>>>(P);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_signal(const SignalTargets &t, cudaStream_t stream) {
     llrl_k_signal<<<1, 32, 0, stream>>>(t);
     return cudaGetLastError();
 }
 
 cudaError_t launch_wait(unsigned long long *flags, const WaitTargets &t, cudaStream_t stream) {
-    llrl_k_wait<<<1, 32, 0, stream>>>(flags, t, 30ull * 1000 * 1000 * 1000);
+    llrl_k_wait<<<1, kNumSlots, 0, stream>>>(flags, t, 30ull * 1000 * 1000 * 1000);
     return cudaGetLastError();
 }
 

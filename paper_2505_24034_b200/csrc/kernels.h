@@ -15,6 +15,7 @@ struct KParams {
     const Seg *segs;
     const TmaRef *tma_refs;            // fp8 items: index i - fp8_base
     const void *tmaps;                 // CUtensorMap array (global memory)
+    const uint32_t *nv_amax;           // NVFP4: global amax (u32 bits) per tensor id, fetched locally
     int fp8_base;
     unsigned long long *done;          // per (plan, device) CTA completion counter (self-resetting), or null
     int item_begin, item_end;          // [begin, end) of this launch
@@ -28,14 +29,54 @@ struct KParams {
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
 constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
-// comm flag buffer words: [0, 16) data arrivals per sender, [16, 32) staging
-// announcements per device, [32] timeout flag, [64, 96) expected counts
-// (device-side, local only).
-constexpr int kFlagTimeout = 2 * kMaxDevices;
-constexpr int kFlagExpected = 4 * kMaxDevices;
-constexpr int kFlagBytes = 8 * 8 * kMaxDevices;
+
+// NVFP4 (R16) per-tensor amax handshake kernels.
+struct NvAmaxParams {
+    const Item *items;
+    int n_items;                       // scan items [0, n_items) (the cast range), F_NV ones count
+    uint32_t *partial;                 // [n_tensors] local partial amax
+    unsigned long long *done;          // self-resetting CTA counter
+    const int32_t *contrib;            // tensor ids this device contributes to
+    int n_contrib;
+    const int32_t *tensor_dev;         // tensor id -> device
+    uint32_t *tables[kMaxDevices];     // amax table of every device (peer-mapped)
+    int my_dev;
+    int n_signal;
+    unsigned long long *signal[kMaxDevices];
+    const void *src[kMaxRanks];
+};
+struct NvScaleParams {
+    const void *locals;                // DeviceWork::NvLocal[n_local]
+    int n_local;
+    uint32_t *table;                   // this device's amax table
+    void *dst[kMaxRanks];
+    int n_signal;
+    unsigned long long *signal[kMaxDevices];
+};
+struct NvFetchParams {
+    const int32_t *contrib;
+    int n_contrib;
+    const int32_t *tensor_dev;
+    const uint32_t *tables[kMaxDevices];
+    uint32_t *amax_out;                // [n_tensors]
+};
+cudaError_t launch_nv_amax(const NvAmaxParams &P, bool src_f32, int grid, cudaStream_t stream);
+cudaError_t launch_nv_scale(const NvScaleParams &P, cudaStream_t stream);
+cudaError_t launch_nv_fetch(const NvFetchParams &P, cudaStream_t stream);
+// comm buffer (u64 words): slot ranges of kMaxDevices counters each --
+// [0,16) data arrivals per sender, [16,32) "layer group staged" per device,
+// [32,48) NVFP4 partial amax arrivals per sender, [48,64) NVFP4 "tensor scales
+// ready" per receiver; [64] timeout flag; [128,192) expected counts per slot
+// (device-side, local); from byte kNvTableOffset: the NVFP4 amax table
+// (17 u32 per tensor: one partial per sender device, then the global amax).
+constexpr int kSlotData = 0, kSlotStaged = 16, kSlotNvAmax = 32, kSlotNvReady = 48, kNumSlots = 64;
+constexpr int kFlagTimeout = 64;
+constexpr int kFlagExpected = 128;
+constexpr int64_t kNvTableOffset = 4096;
+constexpr int64_t kCommBytes = 1 << 20;
+constexpr int kNvTableStride = kMaxDevices + 1;   // u32 per tensor
 struct WaitTargets {
-    unsigned long long count[2 * kMaxDevices];   // arrivals to wait for per flag slot; 0 = none
+    unsigned long long count[kNumSlots];   // arrivals to wait for per flag slot; 0 = none
 };
 struct SignalTargets {
     unsigned long long *slot[kMaxDevices];

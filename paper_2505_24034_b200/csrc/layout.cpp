@@ -25,11 +25,14 @@ void set_error(const char *fmt, ...) {
 
 int64_t dtype_bytes(int dt) { return dt == LLRL_F32 ? 4 : dt == LLRL_BF16 ? 2 : 1; }
 
-int64_t data_bytes(int dt, int64_t elems) { return dt == LLRL_MXFP4 ? elems / 2 : elems * dtype_bytes(dt); }
+int64_t data_bytes(int dt, int64_t elems) {
+    return (dt == LLRL_MXFP4 || dt == LLRL_NVFP4) ? elems / 2 : elems * dtype_bytes(dt);
+}
 
 // R9 / R13 / R15: fp8 blocks -> fp32 [ceil(R/128), ceil(C/128)]; MX -> E8M0 bytes [R, ceil(C/32)].
 int64_t scale_grid_bytes(int dt, int64_t rows, int64_t cols) {
     if (dt == LLRL_MXFP8 || dt == LLRL_MXFP4) return rows * ((cols + kMxGroup - 1) / kMxGroup);
+    if (dt == LLRL_NVFP4) return rows * ((cols + kNvGroup - 1) / kNvGroup);
     return ((rows + kFp8Block - 1) / kFp8Block) * ((cols + kFp8Block - 1) / kFp8Block) * 4;
 }
 
@@ -147,6 +150,9 @@ llrl_status build_dst(llrl_layout *L) {
     if (L->dtype == LLRL_MXFP4 && (m.d_model % kMxGroup || (int64_t(m.n_heads) * m.head_dim / T) % kMxGroup ||
                                    (m.d_ffn / T) % kMxGroup))
         return LLRL_E_UNSUPPORTED;
+    if (L->dtype == LLRL_NVFP4 && (m.d_model % kNvGroup || (int64_t(m.n_heads) * m.head_dim / T) % kNvGroup ||
+                                   (m.d_ffn / T) % kNvGroup))
+        return LLRL_E_UNSUPPORTED;
     const auto &ps = L->src_params;
     auto &dp = L->dst_params;
     dp.clear();
@@ -220,8 +226,8 @@ llrl_status build_dst(llrl_layout *L) {
                 pc.parts.clear();
             }
             pc.rect = Rect{0, pc.rows, 0, pc.cols};
-            pc.quantised = (L->dtype == LLRL_FP8_E4M3 || L->dtype == LLRL_MXFP8 || L->dtype == LLRL_MXFP4) &&
-                           dp[i].quantisable;
+            pc.quantised = (L->dtype == LLRL_FP8_E4M3 || L->dtype == LLRL_MXFP8 || L->dtype == LLRL_MXFP4 ||
+                            L->dtype == LLRL_NVFP4) && dp[i].quantisable;
             pc.dtype = pc.quantised ? L->dtype : (L->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
             off = align_up(off);
             pc.byte_off = off;
@@ -230,6 +236,11 @@ llrl_status build_dst(llrl_layout *L) {
                 off = align_up(off);
                 pc.scale_off = off;
                 off += scale_grid_bytes(L->dtype, pc.rows, pc.cols);
+                if (L->dtype == LLRL_NVFP4) {      // R16: fp32 tensor scale at the next 256-byte boundary
+                    off = align_up(off);
+                    pc.tscale_off = off;
+                    off += 4;
+                }
             }
             L->pieces[size_t(sg)].push_back(pc);
         }
@@ -271,7 +282,7 @@ llrl_status llrl_layout_describe_ex(const llrl_model *m, const llrl_layout_opts 
     const int src_dtype = o->src_dtype, dst_dtype = o->dst_dtype;
     if ((src_dtype != LLRL_F32 && src_dtype != LLRL_BF16) ||
         (dst_dtype != LLRL_F32 && dst_dtype != LLRL_BF16 && dst_dtype != LLRL_FP8_E4M3 && dst_dtype != LLRL_MXFP8 &&
-         dst_dtype != LLRL_MXFP4) ||
+         dst_dtype != LLRL_MXFP4 && dst_dtype != LLRL_NVFP4) ||
         (dst_dtype == LLRL_F32 && src_dtype != LLRL_F32)) {
         set_error("llrl_layout_describe: unsupported dtypes src=%d dst=%d", src_dtype, dst_dtype);
         return LLRL_E_UNSUPPORTED;
@@ -348,6 +359,7 @@ llrl_status llrl_layout_param_view(const llrl_layout *l, int rank, int param, ll
     out->rows = pc.rows; out->cols = pc.cols;
     out->byte_off = pc.byte_off;
     out->scale_off = pc.scale_off;
+    out->tensor_scale_off = pc.tscale_off;
     return LLRL_OK;
 }
 

@@ -111,7 +111,7 @@ struct Builder {
                         t.lc0 = I.c0 - F.c0;
                         t.dst_ld = pc.cols;
                         // element offset in the rank buffer (MXFP4: 4-bit elements)
-                        t.dst_off = (pc.dtype == LLRL_MXFP4 ? 2 * pc.byte_off : pc.byte_off / es_d) +
+                        t.dst_off = ((pc.dtype == LLRL_MXFP4 || pc.dtype == LLRL_NVFP4) ? 2 * pc.byte_off : pc.byte_off / es_d) +
                                     t.lr0 * pc.cols + t.lc0;
                         t.quant = pc.quantised;
                         P->tiles.push_back(t);
@@ -125,8 +125,9 @@ struct Builder {
     void add_cast_items(const Tile &t, std::vector<Item> &out) {
         Item base{};
         base.kind = K_CAST;
-        base.src_rank = uint16_t(t.src_rank);
-        base.dst_rank = uint16_t(t.dst_rank);
+        base.src_rank = uint8_t(t.src_rank);
+        base.dst_rank = uint8_t(t.dst_rank);
+        base.tid = -1;
         const uint16_t fl = D->dtype == LLRL_F32 ? F_DST_F32 : 0;
         const bool contiguous = t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld);
         if (contiguous) {
@@ -138,7 +139,7 @@ struct Builder {
                     it.src_off = s + i; it.dst_off = d + i;
                     it.rows = 1; it.cols = int32_t(std::min(chunk_elems(), len - i));
                     it.src_ld = it.cols; it.dst_ld = it.cols;
-                    it.flags = uint16_t(fl | (vec ? F_VEC : 0));
+                    it.flags = uint8_t(fl | (vec ? F_VEC : 0));
                     out.push_back(it);
                 }
             };
@@ -165,7 +166,7 @@ struct Builder {
             it.dst_ld = int32_t(t.dst_ld);
             it.src_off = t.src_off + r * t.src_ld;
             it.dst_off = t.dst_off + r * t.dst_ld;
-            it.flags = uint16_t(fl | (vec ? F_VEC : 0));
+            it.flags = uint8_t(fl | (vec ? F_VEC : 0));
             out.push_back(it);
         }
     }
@@ -173,17 +174,39 @@ struct Builder {
     // MXFP8 tile -> cast items with F_MX.  Every 1x32 group must lie inside one
     // tile and one item: the tile's columns (or, for a run contiguous on both
     // sides, its whole length) start and end on 32-element group boundaries.
+    std::map<std::pair<int, int>, int32_t> nv_tid;   // (dst rank, dst param) -> NVFP4 tensor id
+
     llrl_status add_mx_items(const Tile &t) {
         const Piece &pc = D->pieces[size_t(t.dst_rank)][size_t(t.dst_param)];
-        const bool fp4 = pc.dtype == LLRL_MXFP4;
+        const bool nv = pc.dtype == LLRL_NVFP4;
+        const bool fp4 = pc.dtype == LLRL_MXFP4 || nv;
+        const int64_t grp = nv ? kNvGroup : kMxGroup;
         const int64_t base = fp4 ? 2 * pc.byte_off : pc.byte_off;   // element offset of the tensor
         const bool contiguous = t.rows == 1 || (t.cols == t.src_ld && t.cols == t.dst_ld);
-        const bool ok = (t.dst_off - base) % kMxGroup == 0 && (contiguous ? (t.rows * t.cols) % kMxGroup == 0
-                                                                          : t.cols % kMxGroup == 0) &&
-                        t.src_off % 8 == 0 && t.src_ld % 8 == 0 && pc.cols % kMxGroup == 0;
+        const bool ok = (t.dst_off - base) % grp == 0 && (contiguous ? (t.rows * t.cols) % grp == 0
+                                                                     : t.cols % grp == 0) &&
+                        t.src_off % 8 == 0 && t.src_ld % 8 == 0 && pc.cols % grp == 0;
         if (!ok) {
-            set_error("MXFP8: tile of generator param %d is not aligned to 1x32 groups", t.dst_param);
+            set_error("MX/NVFP4: tile of generator param %d is not aligned to whole row groups", t.dst_param);
             return LLRL_E_UNSUPPORTED;
+        }
+        int32_t tid = -1;
+        if (nv) {
+            auto key = std::make_pair(t.dst_rank, t.dst_param);
+            auto f = nv_tid.find(key);
+            if (f == nv_tid.end()) {
+                tid = int32_t(P->nv_tensors.size());
+                nv_tid[key] = tid;
+                P->nv_tensors.push_back({int32_t(t.dst_rank), int32_t(t.dst_param),
+                                         int32_t(P->dst_device[size_t(t.dst_rank)]), pc.tscale_off});
+                P->dev[size_t(P->dst_device[size_t(t.dst_rank)])].hbm_write += 4;   // the fp32 tensor scale
+                P->stats.dst_bytes += 4;
+            } else {
+                tid = f->second;
+            }
+            DeviceWork &E = P->dev[size_t(P->src_device[size_t(t.src_rank)])];
+            if (std::find(E.nv_contrib.begin(), E.nv_contrib.end(), tid) == E.nv_contrib.end())
+                E.nv_contrib.push_back(tid);
         }
         std::vector<Item> tmp;
         add_cast_items(t, tmp);
@@ -191,16 +214,17 @@ struct Builder {
         const SrcParam &sp = S->src_params[size_t(t.src_param)];
         auto &L = lists[size_t(sd)][size_t(dd)][size_t(group_of(sp.kind, sp.layer))];
         for (Item it : tmp) {
-            it.flags = uint16_t((it.flags & F_VEC) | F_MX | (fp4 ? F_FP4 : 0));
-            if (!(it.flags & F_VEC) || it.dst_off % kMxGroup != 0) {
-                set_error("MXFP8: unaligned cast item");
+            it.flags = uint8_t((it.flags & F_VEC) | F_MX | (fp4 ? F_FP4 : 0) | (nv ? F_NV : 0));
+            if (!(it.flags & F_VEC) || it.dst_off % grp != 0) {
+                set_error("MX/NVFP4: unaligned cast item");
                 return LLRL_E_UNSUPPORTED;
             }
-            it.aux = pc.scale_off - base / kMxGroup;      // scale byte of element o: aux + o / 32
+            it.aux = pc.scale_off - base / grp;           // scale byte of element o: aux + o / group
+            it.tid = tid;
             L.push_back(it);
         }
         const int64_t n = t.rows * t.cols;
-        account(sd, sd, dd, n * es_src, (fp4 ? n / 2 : n) + n / kMxGroup, false);
+        account(sd, sd, dd, n * es_src, (fp4 ? n / 2 : n) + n / grp, false);
         return LLRL_OK;
     }
 
@@ -273,7 +297,7 @@ struct Builder {
         mc_extra.assign(size_t(G), std::vector<std::vector<int>>(size_t(n_groups)));
         seglists.assign(G, {});
         // bf16 / f32 tiles, and MXFP8 tiles (row-wise 1x32 groups ride on cast items, R13)
-        const bool mx = D->dtype == LLRL_MXFP8 || D->dtype == LLRL_MXFP4;
+        const bool mx = D->dtype == LLRL_MXFP8 || D->dtype == LLRL_MXFP4 || D->dtype == LLRL_NVFP4;
         for (const Tile &t : P->tiles) {
             if (t.quant && !mx) continue;
             if (t.quant) {
@@ -298,7 +322,7 @@ struct Builder {
             for (Item it : tmp) {
                 const int64_t n = int64_t(it.rows) * it.cols;
                 {
-                    it.flags = uint16_t(it.flags | F_MC);
+                    it.flags = uint8_t(it.flags | F_MC);
                     lists[sd][dd][grp].push_back(it);
                     P->dev[size_t(sd)].has_mc = true;
                     account(sd, sd, dd, n * es_src, n * es_dst, false);
@@ -338,7 +362,8 @@ struct Builder {
                         if (!I.empty()) segs.push_back({ti, I});
                     }
                     Item it{};
-                    it.dst_rank = uint16_t(g);
+                    it.dst_rank = uint8_t(g);
+                    it.tid = -1;
                     it.rows = int32_t(B.rows());
                     it.cols = int32_t(B.cols());
                     it.dst_off = pc.byte_off + B.r0 * pc.cols + B.c0;
@@ -349,7 +374,7 @@ struct Builder {
                         const Tile &t = P->tiles[segs[0].first];
                         const int sd = P->src_device[t.src_rank];
                         it.kind = K_FP8;
-                        it.src_rank = uint16_t(t.src_rank);
+                        it.src_rank = uint8_t(t.src_rank);
                         it.src_off = t.src_off + (B.r0 - t.lr0) * t.src_ld + (B.c0 - t.lc0);
                         it.src_ld = int32_t(t.src_ld);
                         const bool vec = it.cols % 16 == 0 && it.src_off % 8 == 0 && it.src_ld % 8 == 0 &&
@@ -362,7 +387,7 @@ struct Builder {
                         P->stats.n_fp8_pull_blocks++;
                         auto &sl = seglists[dd];
                         it.src_off = int64_t(sl.size());
-                        it.src_rank = uint16_t(segs.size());   // segment count
+                        it.src_rank = uint8_t(segs.size());   // segment count
                         for (auto &s : segs) {
                             const Tile &t = P->tiles[s.first];
                             const Rect &I = s.second;
@@ -485,6 +510,17 @@ struct Builder {
                     }
             }
         }
+        // NVFP4 handshake sets: tensors held per device, contributors per device
+        for (int32_t tid = 0; tid < int32_t(P->nv_tensors.size()); tid++)
+            P->dev[size_t(P->nv_tensors[size_t(tid)].device)].nv_local.push_back(tid);
+        for (int e = 0; e < G; e++)
+            for (int32_t tid : P->dev[size_t(e)].nv_contrib) {
+                const int d = P->nv_tensors[size_t(tid)].device;
+                auto &tg = P->dev[size_t(e)].nv_targets;
+                if (std::find(tg.begin(), tg.end(), d) == tg.end()) tg.push_back(d);
+                auto &sn = P->dev[size_t(d)].nv_senders;
+                if (std::find(sn.begin(), sn.end(), e) == sn.end()) sn.push_back(e);
+            }
         // per-group byte ranges of every rank buffer (host <-> device streaming)
         P->src_group_range.assign(size_t(S->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));
         P->dst_group_range.assign(size_t(D->n_ranks), std::vector<std::pair<int64_t, int64_t>>(size_t(n_groups), {-1, -1}));
@@ -533,6 +569,7 @@ llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, con
     P->n_src = src->n_ranks;
     P->n_dst = dst->n_ranks;
     P->multicast = (flags & LLRL_PLAN_MULTICAST) != 0;
+    P->nv = dst->dtype == LLRL_NVFP4;
     P->src_dtype = src->dtype;
     P->dst_dtype = dst->dtype;
     P->src_device.assign(src_device, src_device + P->n_src);

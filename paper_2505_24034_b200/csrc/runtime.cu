@@ -59,6 +59,29 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         CK(cudaMalloc(&W.d_tmaps, W.tma_pieces.size() * 128));
         W.h_tmaps.assign(W.tma_pieces.size() * 128, 0);
     }
+    if (p->nv && !p->nv_tensors.empty()) {
+        const size_t nt = p->nv_tensors.size();
+        CK(cudaMalloc(&W.d_nv_partial, nt * 4));
+        CK(cudaMalloc(&W.d_nv_amax, nt * 4));
+        CK(cudaMemset(W.d_nv_amax, 0, nt * 4));
+        std::vector<int32_t> tdev(nt);
+        for (size_t t = 0; t < nt; t++) tdev[t] = p->nv_tensors[t].device;
+        CK(cudaMalloc(&W.d_nv_tensor_dev, nt * 4));
+        CK(cudaMemcpy(W.d_nv_tensor_dev, tdev.data(), nt * 4, cudaMemcpyHostToDevice));
+        if (!W.nv_contrib.empty()) {
+            CK(cudaMalloc(&W.d_nv_contrib, W.nv_contrib.size() * 4));
+            CK(cudaMemcpy(W.d_nv_contrib, W.nv_contrib.data(), W.nv_contrib.size() * 4, cudaMemcpyHostToDevice));
+        }
+        if (!W.nv_local.empty()) {
+            std::vector<DeviceWork::NvLocal> loc;
+            for (int32_t t : W.nv_local)
+                loc.push_back({t, p->nv_tensors[size_t(t)].dst_rank, p->nv_tensors[size_t(t)].tscale_off});
+            CK(cudaMalloc(&W.d_nv_local, loc.size() * sizeof(DeviceWork::NvLocal)));
+            CK(cudaMemcpy(W.d_nv_local, loc.data(), loc.size() * sizeof(DeviceWork::NvLocal), cudaMemcpyHostToDevice));
+        }
+        CK(cudaMalloc(&W.d_nv_done, 256));
+        CK(cudaMemset(W.d_nv_done, 0, 256));
+    }
     CK(cudaMalloc(&W.d_done, 256));
     CK(cudaMemset(W.d_done, 0, 256));
     int sms = 0;
@@ -157,7 +180,7 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
         return LLRL_E_INVALID;
     }
     DeviceWork &W = p->dev[size_t(device)];
-    bool cross = !W.signal_devices.empty() || W.n_senders_in > 0;
+    bool cross = !W.signal_devices.empty() || W.n_senders_in > 0 || p->nv;   // NVFP4: amax table in the comm
     for (size_t g = 0; g < W.pull_from.size(); g++) cross = cross || !W.pull_from[g].empty() || !W.pull_to[g].empty();
     if (cross) {
         if (!comm || comm->device != device) {
@@ -192,6 +215,7 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
     }
     kp->items = W.d_items;
     kp->segs = W.d_segs;
+    kp->nv_amax = W.d_nv_amax;
     kp->tma_refs = W.d_tma_refs;
     kp->tmaps = W.d_tmaps;
     kp->fp8_base = int(W.n_cast);
@@ -236,6 +260,73 @@ static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &devs, 
     return LLRL_OK;
 }
 
+// NVFP4 (R16) per-tensor amax handshake (see kernels.cu): partials -> owners,
+// owners reduce and publish, contributors fetch; all device-side, stream-ordered.
+static uint32_t *nv_table(llrl_comm *comm, int dev) {
+    return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(comm->peer_flags[dev]) + kNvTableOffset);
+}
+
+static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, int device, const KParams &kp,
+                                cudaStream_t s) {
+    if (p->nv_tensors.size() * kNvTableStride * 4 > size_t(kCommBytes - kNvTableOffset)) {
+        set_error("NVFP4: %zu generator tensors exceed the comm's amax table", p->nv_tensors.size());
+        return LLRL_E_UNSUPPORTED;
+    }
+    for (int d : W.nv_targets)
+        if (!comm->peer_flags[d]) { set_error("NVFP4: no comm mapping for device %d", d); return LLRL_E_NOPEER; }
+    for (int d : W.nv_senders)
+        if (!comm->peer_flags[d]) { set_error("NVFP4: no comm mapping for device %d", d); return LLRL_E_NOPEER; }
+    if (!W.nv_contrib.empty()) {
+        NvAmaxParams a;
+        std::memset(&a, 0, sizeof a);
+        a.items = W.d_items;
+        a.n_items = int(W.n_cast);
+        a.partial = W.d_nv_partial;
+        a.done = W.d_nv_done;
+        a.contrib = W.d_nv_contrib;
+        a.n_contrib = int(W.nv_contrib.size());
+        a.tensor_dev = W.d_nv_tensor_dev;
+        for (int d = 0; d < p->n_devices; d++)
+            if (comm->peer_flags[d]) a.tables[d] = nv_table(comm, d);
+        a.my_dev = device;
+        a.n_signal = int(W.nv_targets.size());
+        for (int i = 0; i < a.n_signal; i++) a.signal[i] = comm->peer_flags[W.nv_targets[size_t(i)]] + kSlotNvAmax + device;
+        for (int r = 0; r < p->n_src; r++) a.src[r] = kp.src[r];
+        CK(cudaMemsetAsync(W.d_nv_partial, 0, p->nv_tensors.size() * 4, s));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 4, W.n_cast)));
+        CK(launch_nv_amax(a, p->src_dtype == LLRL_F32, grid, s));
+    }
+    if (!W.nv_local.empty()) {
+        llrl_status st = wait_arrivals(comm, W.nv_senders, s, kSlotNvAmax);
+        if (st != LLRL_OK) return st;
+        NvScaleParams c;
+        std::memset(&c, 0, sizeof c);
+        c.locals = W.d_nv_local;
+        c.n_local = int(W.nv_local.size());
+        c.table = nv_table(comm, device);
+        for (int g = 0; g < p->n_dst; g++) c.dst[g] = kp.dst[g];
+        c.n_signal = int(W.nv_senders.size());
+        for (int i = 0; i < c.n_signal; i++) c.signal[i] = comm->peer_flags[W.nv_senders[size_t(i)]] + kSlotNvReady + device;
+        CK(launch_nv_scale(c, s));
+    }
+    if (!W.nv_contrib.empty()) {
+        llrl_status st = wait_arrivals(comm, W.nv_targets, s, kSlotNvReady);
+        if (st != LLRL_OK) return st;
+        NvFetchParams f;
+        std::memset(&f, 0, sizeof f);
+        f.contrib = W.d_nv_contrib;
+        f.n_contrib = int(W.nv_contrib.size());
+        f.tensor_dev = W.d_nv_tensor_dev;
+        for (int d = 0; d < p->n_devices; d++)
+            if (comm->peer_flags[d]) f.tables[d] = nv_table(comm, d);
+        f.amax_out = W.d_nv_amax;
+        CK(launch_nv_fetch(f, s));
+    }
+    return LLRL_OK;
+}
+
 llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs, void *const *dst_ptrs,
                       void *stream) {
     DeviceGuard guard(device >= 0 ? device : 0);
@@ -244,6 +335,10 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
     if (st != LLRL_OK) return st;
     DeviceWork &W = p->dev[size_t(device)];
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (p->nv) {
+        st = nv_handshake(p, W, comm, device, kp, s);
+        if (st != LLRL_OK) return st;
+    }
     st = launch_ranges(p, W, comm, kp, 0, W.n_cast, W.n_cast, int64_t(W.items.size()), W.signal_devices, s);
     if (st != LLRL_OK) return st;
     return wait_arrivals(comm, W.senders, s);
@@ -284,6 +379,7 @@ llrl_status llrl_plan_group_range(const llrl_plan *p, int side, int rank, int gr
 llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group, void *const *src_ptrs,
                             void *const *dst_ptrs, void *stream) {
     if (!p || group < 0 || group >= p->n_groups) { set_error("llrl_sync_group: invalid group"); return LLRL_E_INVALID; }
+    if (p->nv) { set_error("llrl_sync_group: NVFP4 needs whole-tensor amax -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
     llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
@@ -301,6 +397,8 @@ llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n) {
     if (!p || !n || device < 0 || device >= p->n_devices) { set_error("invalid argument"); return LLRL_E_INVALID; }
     const DeviceWork &W = p->dev[device];
     *n = (W.n_cast > 0 ? 1 : 0) + (int64_t(W.items.size()) > W.n_cast ? 1 : 0) + (W.n_senders_in > 0 ? 1 : 0);
+    if (p->nv)   // amax, scale (+ wait), fetch (+ wait)
+        *n += (W.nv_contrib.empty() ? 0 : 3) + (W.nv_local.empty() ? 0 : 2);
     return LLRL_OK;
 }
 
@@ -324,6 +422,7 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void *const *host_src,
                            void *const *host_dst, void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
     if (!host_src || !host_dst) { set_error("llrl_sync_host: invalid argument"); return LLRL_E_INVALID; }
+    if (p && p->nv) { set_error("llrl_sync_host: NVFP4 needs whole-tensor amax -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
     llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
@@ -364,13 +463,13 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
             std::memset(&t, 0, sizeof t);
             for (int d : W.pull_to[gg]) {
                 if (!comm || !comm->peer_flags[d]) { set_error("llrl_sync_host: no flag mapping for %d", d); return LLRL_E_NOPEER; }
-                t.slot[t.n++] = comm->peer_flags[d] + kMaxDevices + device;
+                t.slot[t.n++] = comm->peer_flags[d] + kSlotStaged + device;
             }
             CK(launch_signal(t, h2d));
         }
         CK(cudaEventRecord(ev(size_t(2 * g)), h2d));
         CK(cudaStreamWaitEvent(s, ev(size_t(2 * g)), 0));
-        st = wait_arrivals(comm, W.pull_from[gg], s, kMaxDevices);   // their bytes staged
+        st = wait_arrivals(comm, W.pull_from[gg], s, kSlotStaged);   // their bytes staged
         if (st != LLRL_OK) return st;
         st = launch_ranges(p, W, comm, kp, W.cast_off[gg], W.cast_off[gg + 1], W.fp8_off[gg], W.fp8_off[gg + 1],
                            W.group_signal[gg], s);
@@ -403,6 +502,12 @@ void llrl_plan_destroy(llrl_plan *p) {
         cudaFree(W.d_done);
         cudaFree(W.d_tma_refs);
         cudaFree(W.d_tmaps);
+        cudaFree(W.d_nv_partial);
+        cudaFree(W.d_nv_amax);
+        cudaFree(W.d_nv_contrib);
+        cudaFree(W.d_nv_tensor_dev);
+        cudaFree(W.d_nv_local);
+        cudaFree(W.d_nv_done);
         for (void *e : W.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         if (W.h2d_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.h2d_stream));
         if (W.d2h_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.d2h_stream));
@@ -418,8 +523,8 @@ llrl_status llrl_comm_create(int device, llrl_comm **out) {
     if (!c) { set_error("out of host memory"); return LLRL_E_NOMEM; }
     c->device = device;
     DeviceGuard guard(device);
-    cudaError_t e = cudaMalloc(&c->flags, kFlagBytes);
-    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, kFlagBytes);
+    cudaError_t e = cudaMalloc(&c->flags, kCommBytes);
+    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, kCommBytes);
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "llrl_comm_create"); }
     c->peer_flags[device] = c->flags;
     *out = c;

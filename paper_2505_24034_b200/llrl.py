@@ -20,8 +20,8 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 OK, E_INVALID, E_INDIVISIBLE, E_MISMATCH, E_UNSUPPORTED, E_CUDA, E_NOPEER, E_NOMEM = 0, -1, -2, -3, -4, -5, -6, -7
-F32, BF16, FP8_E4M3, MXFP8, MXFP4 = 0, 1, 2, 3, 4
-DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8, "mxfp4": MXFP4}
+F32, BF16, FP8_E4M3, MXFP8, MXFP4, NVFP4 = 0, 1, 2, 3, 4, 5
+DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8, "mxfp4": MXFP4, "nvfp4": NVFP4}
 MESH_FSDP_INNER = 1
 PLAN_MULTICAST = 1
 (P_ATTN_NORM, P_Q, P_K, P_V, P_O, P_MLP_NORM, P_GATE, P_UP, P_DOWN, P_EMBED, P_FINAL_NORM, P_LM_HEAD,
@@ -61,7 +61,8 @@ class ParamView(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("layer", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("quantised", ctypes.c_int32), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
                 ("byte_off", ctypes.c_int64), ("scale_off", ctypes.c_int64), ("full_r0", ctypes.c_int64),
-                ("full_c0", ctypes.c_int64), ("src_param", ctypes.c_int32), ("is_norm", ctypes.c_int32)]
+                ("full_c0", ctypes.c_int64), ("src_param", ctypes.c_int32), ("is_norm", ctypes.c_int32),
+                ("tensor_scale_off", ctypes.c_int64)]
 
 
 class Run(ctypes.Structure):

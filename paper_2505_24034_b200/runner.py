@@ -83,6 +83,8 @@ class SyncJob:
         self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else 0 for g in range(self.D.n_ranks)]
         if self.world > 1:
             self._exchange()
+        elif cfg.dst_dtype == "nvfp4":
+            self.comm = llrl.Comm(self.device)     # NVFP4 keeps its amax table in the comm buffer
 
     # -- setup ---------------------------------------------------------------
     def fill(self, seed: int):

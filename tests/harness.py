@@ -116,3 +116,19 @@ def expected_mx4_group(ol: oracle.Layout, seed, g, gp, r, j):
     if ol.src_dtype == "bf16":
         bits = bits << np.uint32(16)
     return oracle.mx4_block(bits.view(np.float32))
+
+
+def dst_tensor_values(ol: oracle.Layout, seed, g, gp):
+    """The whole generator-local tensor gp of rank g as fp32 (from synth, row by row
+    through the oracle's index mapping) -- for NVFP4's per-tensor scale."""
+    R, C, q, off, soff = ol.dst_param(g, gp)
+    x = np.zeros((R, C), np.float32)
+    for r in range(R):
+        p, row, col = ol.dst_element_source(g, gp, r, 0)
+        is_norm = ol.src_param_info(p)[2] == 2
+        bits = synth.weight_bits(seed, p, is_norm, ol.src_dtype, np.array([row]), np.arange(col, col + C))
+        bits = bits.astype(np.uint32)
+        if ol.src_dtype == "bf16":
+            bits = bits << np.uint32(16)
+        x[r] = bits.view(np.float32)
+    return x

@@ -132,6 +132,8 @@ def main():
         (3, 2, 4, "f32", "f32", "disjoint"),
         (2, 2, 8, "bf16", "mxfp8", "rotated"),
         (2, 2, 8, "f32", "mxfp4", "colocated"),
+        (2, 2, 8, "bf16", "nvfp4", "colocated"),     # per-tensor amax reduced across GPUs
+        (4, 1, 2, "f32", "nvfp4", "disjoint"),
     ]
     for c in cases:
         toy_case(runner, world, *c)

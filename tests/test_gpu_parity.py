@@ -91,6 +91,9 @@ def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
     (2, 2, 8, "bf16", "mxfp8", True),
     (3, 1, 4, "bf16", "mxfp4", False),  # MXFP4 (R15)
     (2, 2, 8, "f32", "mxfp4", True),
+    (2, 1, 2, "f32", "nvfp4", False),   # NVFP4 (R16): per-tensor amax over several trainer ranks
+    (2, 2, 8, "bf16", "nvfp4", True),
+    (3, 1, 4, "bf16", "nvfp4", False),
 ])
 def test_toy_parity_odd(rt, fsdp, tpt, tpg, sdt, ddt, inner):
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, inner)
@@ -119,7 +122,8 @@ def _inject_specials(ol, src):
 
 
 @pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16"),
-                                     ("f32", "mxfp8"), ("bf16", "mxfp8"), ("f32", "mxfp4"), ("bf16", "mxfp4")])
+                                     ("f32", "mxfp8"), ("bf16", "mxfp8"), ("f32", "mxfp4"), ("bf16", "mxfp4"),
+                                     ("f32", "nvfp4"), ("bf16", "nvfp4")])
 def test_toy_parity_special_values(rt, sdt, ddt):
     # tp_train = 1: no replicated trainer pieces, so injected values stay consistent
     job = _toy_job(rt, "toy", 3, 1, 4, sdt, ddt)
@@ -198,6 +202,20 @@ def _sampled_check(job, n_samples=20000, n_blocks=6, seed=0):
             got = got.view(np.uint32 if es == 4 else np.uint16).astype(np.int64)
             want = harness.expected_elements(ol, 0, g, gp, lr, lc)
             assert np.array_equal(got, want), (g, gp)
+        if cfg.dst_dtype == "nvfp4":
+            qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
+            for gp in rng.choice(qparams, min(2, n_blocks), replace=False):
+                R, C, q, off, soff = ol.dst_param(g, int(gp))
+                x = harness.dst_tensor_values(ol, 0, g, int(gp))
+                dec, enc = oracle.nv_tensor_scales(x)
+                tso = ol.dst_tensor_scale_off(g, int(gp))
+                assert t[tso:tso + 4].cpu().numpy().view(np.float32)[0] == dec, (g, gp)
+                nsc = C // 16
+                for r, j in [(0, 0), (R - 1, nsc - 1), (int(rng.integers(R)), int(rng.integers(nsc)))]:
+                    codes, sc = oracle.nv_group(x[r, j * 16:(j + 1) * 16], enc)
+                    b0 = off + (r * C + j * 16) // 2
+                    assert np.array_equal(t[b0:b0 + 8].cpu().numpy(), (codes[0::2] | (codes[1::2] << 4)).astype(np.uint8))
+                    assert int(t[soff + r * nsc + j].item()) == sc, (g, gp, r, j)
         if cfg.dst_dtype == "mxfp4":
             qparams = [gp for gp in range(n_params) if ol.dst_param(g, gp)[2]]
             for gp in rng.choice(qparams, n_blocks, replace=False):
@@ -274,6 +292,15 @@ def test_full_c10_70b_mxfp4_sampled(rt):
     job.sync()
     torch.cuda.synchronize()
     _sampled_check(job, n_samples=4000, n_blocks=4)
+    job.close()
+
+
+def test_full_c11_70b_nvfp4_sampled(rt):
+    """C11 (70B bf16 TP=8 -> NVFP4 TP=8, per-tensor amax handshake) at G=1, 40-layer slice."""
+    job = _full_job(rt, "c11")
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=2000, n_blocks=2)
     job.close()
 
 

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(L):
     (f, tt, tg, "f32", "bf16", False) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)
 ] + [(2, 2, 8, "bf16", "fp8", True), (3, 1, 4, "f32", "fp8", False), (3, 2, 4, "f32", "f32", False),
       (3, 1, 4, "f32", "mxfp8", False), (2, 2, 8, "bf16", "mxfp8", True), (3, 1, 4, "f32", "mxfp4", False),
-      (2, 2, 8, "bf16", "mxfp4", True)])
+      (2, 2, 8, "bf16", "mxfp4", True), (2, 1, 2, "f32", "nvfp4", False), (2, 2, 8, "bf16", "nvfp4", True)])
 def test_layout_matches_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner):
     m = MODELS["toy"]
     S, D = L.describe(m, fsdp, tpt, tpg, sdt, ddt, inner)
@@ -165,7 +165,7 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
     dst = [np.zeros(n, np.uint8) for n in dst_sizes]
     # fp8: assemble generator-local fp32 tensors, then quantise per 128x128 block
     local = {}
-    epb = 2 if dst_dtype == "mxfp4" else 1          # quantised elements per byte
+    epb = 2 if dst_dtype in ("mxfp4", "nvfp4") else 1          # quantised elements per byte
     for r in runs:
         src = src_bufs[r["src_rank"]]
         raw = src[r["src_off"] * es:(r["src_off"] + r["len"]) * es]
@@ -187,8 +187,12 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
             e0 = v.byte_off * epb
             x = d["codes"][e0:e0 + v.rows * v.cols].reshape(v.rows, v.cols)
             assert not np.isnan(x).any()
-            quant = {"mxfp8": brute.mx_quant, "mxfp4": brute.mx4_quant}.get(dst_dtype, brute.fp8_quant)
-            q, s = quant(x)
+            if dst_dtype == "nvfp4":
+                q, s, ts = brute.nv_quant(x)
+                dst[g][v.tensor_scale_off:v.tensor_scale_off + 4] = ts.view(np.uint8)
+            else:
+                quant = {"mxfp8": brute.mx_quant, "mxfp4": brute.mx4_quant}.get(dst_dtype, brute.fp8_quant)
+                q, s = quant(x)
             dst[g][v.byte_off:v.byte_off + q.size] = q.reshape(-1)
             dst[g][v.scale_off:v.scale_off + s.nbytes] = s.view(np.uint8).reshape(-1)
     return dst
@@ -207,6 +211,8 @@ def _interpret(L, plan, D, src_bufs, src_dtype, dst_dtype, dst_sizes):
     (8, 1, 8, "bf16", "mxfp8", False, 8),
     (3, 1, 4, "f32", "mxfp4", False, 2),
     (2, 2, 8, "bf16", "mxfp4", True, 4),
+    (2, 1, 2, "f32", "nvfp4", False, 2),
+    (2, 2, 8, "bf16", "nvfp4", True, 4),
 ])
 def test_plan_runs_reproduce_oracle(L, fsdp, tpt, tpg, sdt, ddt, inner, G):
     m = MODELS["toy"]
@@ -336,8 +342,13 @@ def test_plan_algorithmic_bytes_equal_layout_bytes(L, name):
             v = D.param_view(g, gp)
             n = v.rows * v.cols
             if v.quantised:
-                data = n // 2 if cfg.dst_dtype == "mxfp4" else n
-                scales = -(-v.rows // 128) * -(-v.cols // 128) * 4 if cfg.dst_dtype == "fp8" else v.rows * -(-v.cols // 32)
+                data = n // 2 if cfg.dst_dtype in ("mxfp4", "nvfp4") else n
+                if cfg.dst_dtype == "fp8":
+                    scales = -(-v.rows // 128) * -(-v.cols // 128) * 4
+                elif cfg.dst_dtype == "nvfp4":
+                    scales = v.rows * -(-v.cols // 16) + 4        # E4M3 per 1x16 + fp32 tensor scale
+                else:
+                    scales = v.rows * -(-v.cols // 32)
                 want_dst += data + scales
             else:
                 want_dst += n * {"f32": 4}.get(cfg.dst_dtype, 2)
