@@ -812,9 +812,22 @@ __global__ void __launch_bounds__(kThreads) llrl_k_nv_amax(const __grid_constant
         const char *src = static_cast<const char *>(P.src[it.src_rank]);
         uint32_t amax = 0;
         const int vpr = it.cols * es / 16;               // 16-byte words per row (cols % 16 == 0)
-        for (int v = threadIdx.x; v < it.rows * vpr; v += kThreads) {
-            const int r = v / vpr, c = v - r * vpr;
-            amax = word_amax<SRC_F32>(ld_stream(src + (it.src_off + int64_t(r) * it.src_ld) * es + c * 16), amax);
+        const int nv = it.rows * vpr;
+        constexpr int U = 8;                              // 8 x 16-byte loads in flight per thread
+        for (int v0 = threadIdx.x; v0 < nv; v0 += kThreads * U) {
+            uint4 w[U];
+#pragma unroll
+            for (int k2 = 0; k2 < U; k2++) {
+                const int v = v0 + k2 * kThreads;
+                if (v < nv) {
+                    const int r = v / vpr, c = v - r * vpr;
+                    w[k2] = ld_stream(src + (it.src_off + int64_t(r) * it.src_ld) * es + c * 16);
+                } else {
+                    w[k2] = make_uint4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < U; k2++) amax = word_amax<SRC_F32>(w[k2], amax);
         }
         amax = block_max_u32(amax, s_red[k & 1]);
         if (threadIdx.x == 0) atomicMax(P.partial + it.tid, amax);

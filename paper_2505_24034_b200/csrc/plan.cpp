@@ -225,6 +225,10 @@ struct Builder {
         }
         const int64_t n = t.rows * t.cols;
         account(sd, sd, dd, n * es_src, (fp4 ? n / 2 : n) + n / grp, false);
+        if (nv) {                       // R16: the per-tensor amax pass reads the source once more
+            P->dev[size_t(sd)].hbm_read += n * es_src;
+            P->stats.src_bytes += n * es_src;
+        }
         return LLRL_OK;
     }
 

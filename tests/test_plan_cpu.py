@@ -353,5 +353,11 @@ def test_plan_algorithmic_bytes_equal_layout_bytes(L, name):
             else:
                 want_dst += n * {"f32": 4}.get(cfg.dst_dtype, 2)
     assert st.dst_bytes == want_dst
+    want_src = 0                     # every trainer element is read once per generator rank it feeds
+    for g in range(D.n_ranks):
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            want_src += v.rows * v.cols * {"f32": 4, "bf16": 2}[cfg.src_dtype] * (2 if v.quantised and cfg.dst_dtype == "nvfp4" else 1)
+    assert st.src_bytes == want_src
     dev = [plan.device_bytes(d) for d in range(st.n_devices)]
     assert sum(b["hbm_write"] for b in dev) == st.dst_bytes and sum(b["hbm_read"] for b in dev) == st.src_bytes
