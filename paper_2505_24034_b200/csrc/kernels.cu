@@ -801,37 +801,82 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
 // cleared for the next sync; contributors are signalled.  Phase C
 // (llrl_k_nv_fetch, contributors): copy the global amax of each contributed
 // tensor into a local array the quantising kernel reads.
+// Phase A streams the source through shared memory with bulk copies (one
+// producer warp keeps kNvStages x 32 KiB in flight across item boundaries, as
+// in llrl_k_cast_tma) and 8 reducer warps take max |x|.  Each CTA owns a
+// contiguous range of items: consecutive items mostly belong to one tensor, so
+// a CTA publishes one partial per tensor run (one atomic per warp) -- no
+// same-address atomic storms.
+constexpr int kNvStageBytes = 32 * 1024, kNvStages = 4;
 template <bool SRC_F32>
-__global__ void __launch_bounds__(kThreads) llrl_k_nv_amax(const __grid_constant__ NvAmaxParams P) {
-    __shared__ uint32_t s_red[2][kThreads / 32];
+__global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_nv_amax(const __grid_constant__ NvAmaxParams P) {
     constexpr int es = SRC_F32 ? 4 : 2;
-    int k = 0;
-    for (int i = blockIdx.x; i < P.n_items; i += gridDim.x) {
-        const Item it = P.items[i];
-        if (!(it.flags & F_NV)) continue;
-        const char *src = static_cast<const char *>(P.src[it.src_rank]);
-        uint32_t amax = 0;
-        const int vpr = it.cols * es / 16;               // 16-byte words per row (cols % 16 == 0)
-        const int nv = it.rows * vpr;
-        constexpr int U = 8;                              // 8 x 16-byte loads in flight per thread
-        for (int v0 = threadIdx.x; v0 < nv; v0 += kThreads * U) {
-            uint4 w[U];
-#pragma unroll
-            for (int k2 = 0; k2 < U; k2++) {
-                const int v = v0 + k2 * kThreads;
-                if (v < nv) {
-                    const int r = v / vpr, c = v - r * vpr;
-                    w[k2] = ld_stream(src + (it.src_off + int64_t(r) * it.src_ld) * es + c * 16);
-                } else {
-                    w[k2] = make_uint4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int k2 = 0; k2 < U; k2++) amax = word_amax<SRC_F32>(w[k2], amax);
+    extern __shared__ __align__(128) unsigned char stages[];
+    __shared__ __align__(8) uint64_t full_bar[kNvStages], empty_bar[kNvStages];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kNvStages; st++) {
+            mbar_init(&full_bar[st], 1);
+            mbar_init(&empty_bar[st], kThreads / 32);
         }
-        amax = block_max_u32(amax, s_red[k & 1]);
-        if (threadIdx.x == 0) atomicMax(P.partial + it.tid, amax);
-        k++;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int per = (P.n_items + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * per, i1 = min(P.n_items, i0 + per);
+    if (warp == kThreads / 32) {
+        // producer
+        int n = 0;
+        for (int i = i0; i < i1; i++) {
+            const Item it = P.items[i];
+            if (!(it.flags & F_NV)) continue;
+            int rows_per, segs;
+            const int nch = cast_chunks<kNvStageBytes>(it, es, &rows_per, &segs);
+            const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kNvStages;
+                mbar_wait(&empty_bar[st], ((n / kNvStages) & 1) ^ 1);
+                const Chunk c = cast_chunk<kNvStageBytes>(it, es, rows_per, segs, k);
+                if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
+                __syncwarp();
+                unsigned char *dst = stages + st * kNvStageBytes;
+                for (int r = lane; r < c.nr; r += 32)
+                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                             uint32_t(c.nc * es), &full_bar[st]);
+            }
+        }
+    } else {
+        // reducers
+        uint32_t amax = 0;
+        int cur = -1, n = 0;
+        for (int i = i0; i < i1; i++) {
+            const Item it = P.items[i];
+            if (!(it.flags & F_NV)) continue;
+            if (it.tid != cur) {
+                if (cur >= 0) {
+                    amax = __reduce_max_sync(0xffffffffu, amax);
+                    if (lane == 0 && amax) atomicMax(P.partial + cur, amax);
+                }
+                amax = 0;
+                cur = it.tid;
+            }
+            int rows_per, segs;
+            const int nch = cast_chunks<kNvStageBytes>(it, es, &rows_per, &segs);
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kNvStages;
+                const Chunk c = cast_chunk<kNvStageBytes>(it, es, rows_per, segs, k);
+                const int nw = c.nr * c.nc * es / 16;
+                mbar_wait(&full_bar[st], (n / kNvStages) & 1);
+                const uint4 *w = reinterpret_cast<const uint4 *>(stages + st * kNvStageBytes);
+                for (int v = threadIdx.x; v < nw; v += kThreads) amax = word_amax<SRC_F32>(w[v], amax);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[st]);
+            }
+        }
+        if (cur >= 0) {
+            amax = __reduce_max_sync(0xffffffffu, amax);
+            if (lane == 0 && amax) atomicMax(P.partial + cur, amax);
+        }
     }
     __threadfence();
     __syncthreads();
@@ -844,7 +889,7 @@ __global__ void __launch_bounds__(kThreads) llrl_k_nv_amax(const __grid_constant
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int j = threadIdx.x; j < P.n_contrib; j += kThreads) {
+    for (int j = threadIdx.x; j < P.n_contrib; j += blockDim.x) {
         const int tid = P.contrib[j];
         const uint32_t v = atomicAdd(P.partial + tid, 0u);      // coherent read of the partial
         P.tables[P.tensor_dev[tid]][tid * kNvTableStride + P.my_dev] = v;
@@ -981,8 +1026,12 @@ cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, i
 }
 
 cudaError_t launch_nv_amax(const NvAmaxParams &P, bool src_f32, int grid, cudaStream_t stream) {
-    if (src_f32) llrl_k_nv_amax<true><<<grid, kThreads, 0, stream>>>(P);
-    else llrl_k_nv_amax<false><<<grid, kThreads, 0, stream>>>(P);
+    constexpr int smem = kNvStages * kNvStageBytes;
+    const void *fn = src_f32 ? (const void *)llrl_k_nv_amax<true> : (const void *)llrl_k_nv_amax<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (src_f32) llrl_k_nv_amax<true><<<grid, kThreads + 32, smem, stream>>>(P);
+    else llrl_k_nv_amax<false><<<grid, kThreads + 32, smem, stream>>>(P);
     return cudaGetLastError();
 }
 

@@ -295,7 +295,7 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
         CK(cudaMemsetAsync(W.d_nv_partial, 0, p->nv_tensors.size() * 4, s));
         int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 4, W.n_cast)));
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(sms), W.n_cast)));   // 1 CTA / SM
         CK(launch_nv_amax(a, p->src_dtype == LLRL_F32, grid, s));
     }
     if (!W.nv_local.empty()) {
