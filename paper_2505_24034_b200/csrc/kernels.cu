@@ -239,6 +239,18 @@ __device__ __forceinline__ float e4m3_value(uint32_t code) {
     return (code & 0x80) ? -v : v;
 }
 
+// x / 6 correctly rounded (fp32 RN) for x >= 0: q = x * RN(1/6) and one fma
+// correction (Markstein), exact for every float in [2^-100, FLT_MAX] (it is
+// not near the subnormal range: those, inf and NaN take the full division).
+// Exhaustively checked against the RN quotient by tests/test_arith_cpu.py.
+__device__ __forceinline__ float div6_rn(float x) {
+    constexpr float y = 0x1.555556p-3f;              // RN(1/6)
+    if (!(x >= 0x1p-100f && x <= 0x1.fffffep127f)) return __fdiv_rn(x, 6.0f);
+    const float q = __fmul_rn(x, y);
+    const float r = __fmaf_rn(-6.0f, q, x);
+    return __fmaf_rn(r, y, q);
+}
+
 // 16 source elements (W words) -> 16 e2m1 codes, two per byte, the even
 // element in the low nibble (cvt.e2m1x2 puts its first operand in the high nibble).
 template <bool SRC_F32, int W>
@@ -598,6 +610,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
     constexpr int kOut = kCastStageBytes / 2;   // bf16, MXFP8 or MXFP4 codes of a chunk
     constexpr int kStride = kCastStageBytes + kOut;
     __shared__ __align__(8) uint64_t full_bar[kCastStages], conv_bar[kCastStages], empty_bar[kCastStages];
+    __shared__ float nv_r[2][128], nv_senc[2];   // NVFP4: r per E4M3 code, S_enc (R16)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kCastStages; s++) {
@@ -683,6 +696,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         // workers
         const int wt = threadIdx.x - 64;
         int n = 0;
+        int nv_tid = -1, nv_buf = 0;
         for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
             const Item it = P.items[i];
             const bool dst_f32 = it.flags & F_DST_F32;
@@ -714,6 +728,22 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
+            if ((it.flags & F_NV) && it.tid != nv_tid) {
+                // R16, per generator tensor: S_enc = 2688 / max(A, 2^-64), and for every
+                // E4M3 group-scale code c the element multiplier r(c) = S_enc / s_q(c)
+                // (0 for s_q = 0) -- one exact division per code instead of per group.
+                // Double-buffered: a worker one tensor ahead writes the other table.
+                nv_tid = it.tid;
+                nv_buf ^= 1;
+                const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
+                const float s_enc = __fdiv_rn(2688.0f, A);
+                if (wt < 128) {
+                    const float sq = e4m3_value(uint32_t(wt));
+                    nv_r[nv_buf][wt] = (wt == 0 || wt == 127) ? 0.0f : __fdiv_rn(s_enc, sq);
+                }
+                if (wt == 0) nv_senc[nv_buf] = s_enc;
+                asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
+            }
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&full_bar[st], (n / kCastStages) & 1);
@@ -731,14 +761,12 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                         }
                     } else {
                         const bool nv = it.flags & F_NV;
-                        float s_enc = 0.0f;
-                        if (nv) {   // R16: S_enc = 2688 / max(A, 2^-64) from the tensor's global amax
-                            const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
-                            s_enc = __fdiv_rn(2688.0f, A);
-                        }
                         // MX (R13 / R15): lanes (2j, 2j+1) hold the two halves of one 1x32 group;
                         // NVFP4 (R16): each thread's 16 elements are one 1x16 group
                         const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
+                        // NVFP4 scale byte of unit u: nv_s0 + u, plus nv_gap per chunk row
+                        const int64_t nv_s0 = it.aux + (it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) / kNvGroup;
+                        const int nv_gap = c.nr > 1 ? int((it.dst_ld - c.nc) / kNvGroup) : 0;
                         for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
                             const int u = u0 + wt;
                             const bool live = u < nunits;
@@ -752,15 +780,15 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             }
                             if (nv) {
                                 // group scale s = (amax / 6) * S_enc -> E4M3 code; r = S_enc / s_q
-                                const float t6 = __fdiv_rn(__uint_as_float(amax), 6.0f);
-                                const uint32_t sc = e4m3x2_rn(__fmul_rn(t6, s_enc), 0.0f) & 0xFFu;
-                                const float sq = e4m3_value(sc);
-                                const float r = sq == 0.0f ? 0.0f : __fdiv_rn(s_enc, sq);
+                                const float t6 = div6_rn(__uint_as_float(amax));
+                                const uint32_t sc = e4m3x2_rn(__fmul_rn(t6, nv_senc[nv_buf]), 0.0f) & 0xFFu;
+                                const float r = nv_r[nv_buf][sc];
                                 if (live) {
                                     reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, r);
-                                    const int e0 = u * 16, rr = e0 / c.nc, cc = e0 - rr * c.nc;
-                                    const int64_t o = it.dst_off + int64_t(c.r0 + rr) * it.dst_ld + c.c0 + cc;
-                                    dbase[it.aux + o / kNvGroup] = static_cast<char>(sc);
+                                    // group index: dst_off, dst_ld and c0 are multiples of 16
+                                    int64_t g = nv_s0 + u;
+                                    if (nv_gap) g += int64_t(u / (c.nc / kNvGroup)) * nv_gap;
+                                    dbase[g] = static_cast<char>(sc);
                                 }
                                 continue;
                             }
