@@ -192,6 +192,21 @@ __device__ __forceinline__ uint32_t max_bf16x2(uint32_t a, uint32_t b) {
     return r;
 }
 
+// max(|a|, |b|) per bf16 half; the sign bits are junk (xor of the inputs'),
+// cleared by the caller.  NaN inputs lose to numbers, as with max.bf16x2.
+__device__ __forceinline__ uint32_t maxabs_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// |x| max of two 16-byte words of bf16 (16 elements) as an fp32 bit pattern.
+__device__ __forceinline__ uint32_t amax16_bf16(const uint4 &a, const uint4 &b) {
+    const uint32_t m = maxabs_bf16x2(maxabs_bf16x2(maxabs_bf16x2(a.x, a.y), maxabs_bf16x2(a.z, a.w)),
+                                     maxabs_bf16x2(maxabs_bf16x2(b.x, b.y), maxabs_bf16x2(b.z, b.w))) &
+                       0x7FFF7FFFu;
+    return max(m << 16, m & 0xFFFF0000u);
+}
+
 template <bool SRC_F32>
 __device__ __forceinline__ uint32_t word_amax(uint4 w, uint32_t amax) {
     if (SRC_F32) {
@@ -203,6 +218,29 @@ __device__ __forceinline__ uint32_t word_amax(uint4 w, uint32_t amax) {
     constexpr uint32_t m = 0x7FFF7FFFu;
     const uint32_t p = max_bf16x2(max_bf16x2(w.x & m, w.y & m), max_bf16x2(w.z & m, w.w & m));
     return max(amax, max(p << 16, p & 0xFFFF0000u));
+}
+
+// (a, b) * r on the packed fp32x2 datapath (sm_100: one instruction, both
+// products fp32 RN, identical to two __fmul_rn).
+__device__ __forceinline__ void mul2_rn(float &a, float &b, float r) {
+    asm("{\n .reg .b64 x, s;\n mov.b64 x, {%0, %1};\n mov.b64 s, {%2, %2};\n"
+        " mul.rn.f32x2 x, x, s;\n mov.b64 {%0, %1}, x;\n}"
+        : "+f"(a), "+f"(b)
+        : "f"(r));
+}
+
+// 8 products -> 4 bytes of e2m1 codes (element 2i in the low nibble of byte i).
+__device__ __forceinline__ uint32_t e2m1x8_rn(const float *y) {
+    uint32_t d;
+    asm("{\n .reg .b8 c0, c1, c2, c3;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 c0, %2, %1;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 c1, %4, %3;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 c2, %6, %5;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 c3, %8, %7;\n"
+        " mov.b32 %0, {c0, c1, c2, c3};\n}"
+        : "=r"(d)
+        : "f"(y[0]), "f"(y[1]), "f"(y[2]), "f"(y[3]), "f"(y[4]), "f"(y[5]), "f"(y[6]), "f"(y[7]));
+    return d;
 }
 
 // 16 source elements (W words) -> 16 e4m3 codes (one 16-byte word).
@@ -222,13 +260,11 @@ __device__ __forceinline__ uint4 quant16(const uint4 *w, float inv) {
             }
         }
     }
+#pragma unroll
+    for (int i = 0; i < 8; i++) mul2_rn(x[2 * i], x[2 * i + 1], inv);
     uint32_t ow[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const uint32_t lo = e4m3x2_rn(__fmul_rn(x[4 * i], inv), __fmul_rn(x[4 * i + 1], inv));
-        const uint32_t hi = e4m3x2_rn(__fmul_rn(x[4 * i + 2], inv), __fmul_rn(x[4 * i + 3], inv));
-        ow[i] = lo | (hi << 16);
-    }
+    for (int i = 0; i < 4; i++) ow[i] = e4m3x2_rn(x[4 * i], x[4 * i + 1]) | (e4m3x2_rn(x[4 * i + 2], x[4 * i + 3]) << 16);
     return make_uint4(ow[0], ow[1], ow[2], ow[3]);
 }
 
@@ -269,16 +305,9 @@ __device__ __forceinline__ uint2 quant16_e2m1(const uint4 *w, float inv) {
             }
         }
     }
-    uint32_t ow[2] = {0, 0};
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        uint32_t b;
-        asm("{ .reg .b8 t; cvt.rn.satfinite.e2m1x2.f32 t, %1, %2; cvt.u32.u8 %0, t; }"
-            : "=r"(b)
-            : "f"(__fmul_rn(x[2 * i + 1], inv)), "f"(__fmul_rn(x[2 * i], inv)));
-        ow[i / 4] |= b << (8 * (i % 4));
-    }
-    return make_uint2(ow[0], ow[1]);
+    for (int i = 0; i < 8; i++) mul2_rn(x[2 * i], x[2 * i + 1], inv);
+    return make_uint2(e2m1x8_rn(x), e2m1x8_rn(x + 8));
 }
 
 // Single-source block, thread t covers rows (t/8) + 32k, k < 4, columns
@@ -767,6 +796,8 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                         // NVFP4 scale byte of unit u: nv_s0 + u, plus nv_gap per chunk row
                         const int64_t nv_s0 = it.aux + (it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) / kNvGroup;
                         const int nv_gap = c.nr > 1 ? int((it.dst_ld - c.nc) / kNvGroup) : 0;
+                        const int64_t mx_s0 = it.aux + (it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) / kMxGroup;
+                        const int mx_gap = c.nr > 1 ? int((it.dst_ld - c.nc) / kMxGroup) : 0;
                         for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
                             const int u = u0 + wt;
                             const bool live = u < nunits;
@@ -774,9 +805,13 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             uint4 w[W];
                             uint32_t amax = 0;
 #pragma unroll
-                            for (int j = 0; j < W; j++) {
+                            for (int j = 0; j < W; j++)
                                 w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
-                                amax = word_amax<SRC_F32>(w[j], amax);
+                            if (SRC_F32) {
+#pragma unroll
+                                for (int j = 0; j < W; j++) amax = word_amax<SRC_F32>(w[j], amax);
+                            } else {
+                                amax = amax16_bf16(w[0], w[W - 1]);
                             }
                             if (nv) {
                                 // group scale s = (amax / 6) * S_enc -> E4M3 code; r = S_enc / s_q
@@ -800,10 +835,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             if (live) {
                                 if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
                                 else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
-                                if ((u & 1) == 0) {
-                                    const int e0 = u * 16, r = e0 / c.nc, cc = e0 - r * c.nc;
-                                    const int64_t o = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0 + cc;
-                                    dbase[it.aux + o / kMxGroup] = static_cast<char>(code);
+                                if ((u & 1) == 0) {   // group index as for NVFP4, 32-element groups
+                                    int64_t g = mx_s0 + (u >> 1);
+                                    if (mx_gap) g += int64_t(u / (c.nc / 16)) * mx_gap;
+                                    dbase[g] = static_cast<char>(code);
                                 }
                             }
                         }
