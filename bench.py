@@ -233,7 +233,7 @@ def run_llrl(args):
     if args.placement:
         import dataclasses
         spec = runner.JobSpec(dataclasses.replace(spec.cfg, placement=args.placement), spec.n_gpus, spec.n_layers)
-    job = runner.SyncJob(spec, device=local, seed=0, multicast=args.multicast)
+    job = runner.SyncJob(spec, device=local, seed=0, multicast=args.multicast, replicate=args.replicate)
     if args.max_ctas:
         job.plan.set_max_ctas(job.device, args.max_ctas)
     cfg = job.cfg
@@ -248,16 +248,36 @@ def run_llrl(args):
     with ClockSampler([local]) as clk:
         time.sleep(0.25)       # let the sampler start before the timed region
         _barrier()
-        with torch.cuda.stream(stream):
-            ev[0].record(stream)
+        if args.step_sync:
+            # isolated syncs: every GPU idle and every rank past a barrier before each
+            # one, so no sync overlaps the previous one's tail (single-sync latency)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
             for k in range(args.steps):
-                job.sync()
-                ev[k + 1].record(stream)
+                torch.cuda.synchronize()
+                _barrier()
+                with torch.cuda.stream(stream):
+                    evs[k][0].record(stream)
+                    job.sync()
+                    evs[k][1].record(stream)
+            torch.cuda.synchronize()
+            _barrier()
+        else:
+            with torch.cuda.stream(stream):
+                ev[0].record(stream)
+                for k in range(args.steps):
+                    job.sync()
+                    ev[k + 1].record(stream)
         _barrier()
-    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
-    ms = _allmax(total_ms / args.steps)
-    ms_min = _allmax(min(step_ms))
+    if args.step_sync:
+        step_ms = [_allmax(a.elapsed_time(b)) for a, b in evs]
+        ms = sum(step_ms) / len(step_ms)
+        ms_min = min(step_ms)
+    else:
+        step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+        total_ms = ev[0].elapsed_time(ev[-1])
+        ms = _allmax(total_ms / args.steps)
+        ms_min = _allmax(min(step_ms))
     launches = int(_allsum(job.num_launches() * args.steps))
 
     # roofline: the binding resource of the binding GPU (the plan is identical on
@@ -265,7 +285,8 @@ def run_llrl(args):
     # algorithmic bytes per sync / the max-over-ranks device time per sync.
     hbm_peak, peak_src = _peaks()
     best = None
-    for d in range(args.gpus):
+    ndev = job.plan.stats().n_devices           # < n_gpus when GPUs only take NCCL replicas
+    for d in range(ndev):
         b = job.plan.device_bytes(d)
         for res, nbytes, peak in (("hbm", b["hbm_read"] + b["hbm_write"], hbm_peak),
                                   ("nvlink", max(b["nvl_tx"], b["nvl_rx"]), NVLINK_PEER_GBS)):
@@ -277,7 +298,7 @@ def run_llrl(args):
             "peak_source": peak_src if res == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = _ncu_traffic(args.config, args.gpus)
-    info = job.plan.device_info(job.device)
+    info = job.plan.device_info(bdev)
     kern = []
     if info.n_cast_items:
         kern.append("llrl_k_cast_tma (TMA-staged relayout + RNE cast, push)")
@@ -286,10 +307,12 @@ def run_llrl(args):
     roof["kernel"] = " + ".join(kern) + f"; whole sync of GPU {bdev} (binding), CUDA events on its stream"
     roof["t_lb_ms"] = round(t_lb, 3)
     roof["binding_gpu"] = bdev
+    if args.replicate == "nccl":
+        roof["note"] = "bytes of the fused replica-0 sync only; the NCCL broadcasts come on top"
 
     # end to end through the C ABI with host buffers (pinned), copies in the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.replicate == "push":   # sync_host has no NCCL-replica stage
         e2e = _e2e(job, args)
 
     comp = _nccl_comparator(job, args) if (args.comparator and args.gpus > 1) else None
@@ -299,7 +322,7 @@ def run_llrl(args):
     tr = job.plan.traffic()
     wire = sum(tr[i][j] for i in range(len(tr)) for j in range(len(tr)) if i != j)
     nvl_per_gpu = max(max(job.plan.device_bytes(d)["nvl_tx"], job.plan.device_bytes(d)["nvl_rx"])
-                      for d in range(args.gpus)) / (ms * 1e6)
+                      for d in range(ndev)) / (ms * 1e6)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
@@ -310,6 +333,8 @@ def run_llrl(args):
                        "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
                        "max_ctas": args.max_ctas or "all SMs",
                        "multicast": bool(args.multicast and job.mc_positions()[0]),
+                       "replicate": args.replicate,
+                       "timing": "isolated syncs (barrier before each)" if args.step_sync else "back-to-back syncs",
                        "n_layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
                        "l2": "inputs >> 126 MB L2 (no flush needed)"},
@@ -473,6 +498,10 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="override decoder layers (profiling only)")
     ap.add_argument("--placement", default=None, choices=["disjoint", "colocated", "rotated", "fanout"])
     ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")
+    ap.add_argument("--step-sync", action="store_true",
+                    help="synchronize + barrier before every timed sync (isolated single-sync latency)")
+    ap.add_argument("--replicate", default="push", choices=["push", "nccl"],
+                    help="generator DP replicas: fused pushes, or replica 0 + NCCL broadcast (a5)")
     ap.add_argument("--comparator", action="store_true", help="also time an NCCL all-to-all-v of the same bytes")
     ap.add_argument("--overlap", action="store_true", help="also time per-layer optimizer/sync overlap (f3)")
     ap.add_argument("--max-ctas", type=int, default=0, help="cap the sync kernels' CTAs per GPU (0 = all SMs)")

@@ -46,7 +46,7 @@ class SyncJob:
     one, the job must fit one device (n_gpus == 1)."""
 
     def __init__(self, spec: JobSpec, device: int | None = None, seed: int = 0, fill: bool = True,
-                 multicast: bool = False):
+                 multicast: bool = False, replicate: str = "push"):
         self.spec = spec
         self.cfg = cfg = spec.cfg
         self.model = spec.model()
@@ -62,7 +62,23 @@ class SyncJob:
         self.S, self.D = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype,
                                        cfg.dst_dtype, cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
         self.src_dev, self.dst_dev = placement(cfg, spec.n_gpus)
-        self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev, multicast=multicast)
+        # generator DP replicas as a plain replication.  "push" (and
+        # multicast) write every replica from the trainer shards in the fused kernels;
+        # "nccl" fills replica 0 with them and NCCL-broadcasts it to the others.
+        if replicate not in ("push", "nccl"):
+            raise ValueError(f"replicate must be 'push' or 'nccl', not {replicate!r}")
+        self.replicate = replicate
+        self._bcast = []
+        if replicate == "nccl":
+            if multicast or cfg.dp_gen < 2:
+                raise ValueError("replicate='nccl' needs dp_gen >= 2 and no multicast")
+            ns = self.D.n_ranks // cfg.dp_gen
+            self.bcast_plan = broadcast_plan(self.dst_dev, cfg.dp_gen)
+            self.D0 = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype,
+                                    cfg.fsdp_inner, 1, cfg.pp_train, cfg.pp_gen)[1]
+            self.plan = llrl.Plan(self.S, self.D0, self.src_dev, self.dst_dev[:ns])
+        else:
+            self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev, multicast=multicast)
         dev = torch.device("cuda", self.device)
         self.src = {r: torch.empty(self.S.rank_bytes(r), dtype=torch.uint8, device=dev)
                     for r in range(self.S.n_ranks) if self.src_dev[r] == self.device}
@@ -83,6 +99,10 @@ class SyncJob:
         self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else 0 for g in range(self.D.n_ranks)]
         if self.world > 1:
             self._exchange()
+            if replicate == "nccl":
+                self._bcast = make_broadcast_groups(_dist(), self.bcast_plan)
+        elif replicate == "nccl":
+            raise ValueError("replicate='nccl' needs one process per GPU")
         elif cfg.dst_dtype == "nvfp4":
             self.comm = llrl.Comm(self.device)     # NVFP4 keeps its amax table in the comm buffer
 
@@ -194,6 +214,13 @@ class SyncJob:
     # -- the hot path ----------------------------------------------------------
     def sync(self, stream=None):
         s = stream if stream is not None else self.stream
+        if self.replicate == "nccl":
+            ns = self.plan.n_dst
+            if self._in_plan():          # a GPU holding only replicas 1.. has no fused work
+                self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs[:ns], s.cuda_stream)
+            with torch.cuda.stream(s):
+                run_broadcasts(_dist(), self._bcast, self.device, self.dst)
+            return
         self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
     def sync_group(self, group, stream=None):
@@ -232,8 +259,11 @@ class SyncJob:
         hd = [host_dst[g].data_ptr() if g in host_dst else 0 for g in range(self.D.n_ranks)]
         self.plan.sync_host(self.comm, self.device, hs, hd, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
+    def _in_plan(self):
+        return self.device in set(self.plan.src_device) | set(self.plan.dst_device)
+
     def num_launches(self):
-        return self.plan.num_launches(self.device)
+        return self.plan.num_launches(self.device) if self._in_plan() else 0
 
     def close(self):
         for p, off in self._opened:
@@ -286,6 +316,47 @@ def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener):
                     bases[h] = opener(h)
                 ptrs[int(r)] = bases[h] + off
     return flags
+
+
+def broadcast_plan(dst_dev, dp):
+    """NCCL replication of generator DP replicas: for every rank
+    position pos of a replica (R12 numbering q = d*ns + pos), the broadcast from
+    replica 0's GPU to the GPUs of replicas 1..dp-1.  Returns [(pos, root GPU,
+    sorted GPUs, {GPU: generator rank})].  Replicas of one position must sit on
+    pairwise different GPUs (one process per GPU).  Pure host logic."""
+    n = len(dst_dev)
+    if dp < 2 or n % dp:
+        raise ValueError("broadcast_plan: need dp >= 2 dividing the generator ranks")
+    ns = n // dp
+    out = []
+    for pos in range(ns):
+        devs = [dst_dev[d * ns + pos] for d in range(dp)]
+        if len(set(devs)) != dp:
+            raise ValueError(f"broadcast_plan: replicas of generator position {pos} share a GPU ({devs})")
+        out.append((pos, devs[0], sorted(devs), {dev: d * ns + pos for d, dev in enumerate(devs)}))
+    return out
+
+
+def make_broadcast_groups(dist, bplan):
+    """One process group per distinct GPU set (created collectively, same order
+    on every process); process rank == GPU ordinal.  [(root, group, {GPU: q})]."""
+    cache = {}
+    out = []
+    for pos, root, devs, ranks in bplan:
+        key = tuple(devs)
+        if key not in cache:
+            cache[key] = dist.new_group(list(key))
+        out.append((root, cache[key], ranks))
+    return out
+
+
+def run_broadcasts(dist, groups, my_dev, bufs):
+    """Enqueue the replica broadcasts this process takes part in (stream-ordered
+    after the sync that filled replica 0 on the root)."""
+    for root, grp, ranks in groups:
+        q = ranks.get(my_dev)
+        if q is not None:
+            dist.broadcast(bufs[q], src=root, group=grp)
 
 
 def spec_for(name: str, n_gpus: int) -> JobSpec:

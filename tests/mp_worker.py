@@ -101,6 +101,28 @@ def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, se
     job.close()
 
 
+def nccl_replica_case(runner, world, fsdp, tpt, tpg, sdt, ddt, dp, seed=21):
+    """a5: replica 0 filled by the fused kernels, replicas 1.. by NCCL broadcast."""
+    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, "colocated", dp_gen=dp)
+    job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False, replicate="nccl")
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, False, dp)
+    for rep in range(2):
+        src = harness.host_src(ol, seed + rep)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x5A)
+        torch.cuda.synchronize()
+        dist.barrier()
+        job.sync()
+        torch.cuda.synchronize()
+        dist.barrier()
+        want = harness.oracle_dst(ol, src, 0x5A)
+        for g, t in job.dst.items():
+            assert np.array_equal(t.cpu().numpy(), want[g]), f"{cfg} nccl replicate rep {rep}: dst rank {g}"
+    job.close()
+
+
 def full_case(runner, world, name):
     from tests.test_gpu_parity import _sampled_check
     spec = runner.spec_for(name, world)
@@ -115,6 +137,10 @@ def full_case(runner, world, name):
     dist.barrier()
     _sampled_check(job, n_samples=4000, n_blocks=3)
     job.close()
+
+
+def rank0():
+    return dist.get_rank() == 0
 
 
 def main():
@@ -150,6 +176,10 @@ def main():
     toy_case(runner, world, world, 1, 1, "f32", "bf16", "colocated", dp=world, multicast=True)
     toy_case(runner, world, 3, 1, 2, "bf16", "bf16", "colocated", dp=world // 2 if world >= 4 else 2,
              multicast=True)
+    nccl_replica_case(runner, world, 2, 1, 1, "f32", "bf16", world)       # a5 NCCL replication
+    nccl_replica_case(runner, world, 2, 2, 2, "bf16", "fp8", world)
+    if rank0():
+        print("ok nccl replicas", flush=True)
     if "--full" in sys.argv:
         for name in ("c2", "c3", "c4", "c5", "c7", "c8", "c10"):
             full_case(runner, world, name)

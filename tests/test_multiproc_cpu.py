@@ -72,6 +72,26 @@ def _worker(rank, world, port, q):
             for g in range(D.n_ranks):
                 if dd[g] != rank:
                     assert dst_ptrs[g] == 10 ** 9 * (dd[g] + 1) + 5000 + 1000 * g
+        # a5 NCCL-style replica broadcast (runner.broadcast_plan / run_broadcasts) on gloo:
+        # replica 0's buffers reach every replica, other ranks' buffers stay untouched
+        import torch
+        for dp, ns in ((world, 1), (world, 2), (2, 3)):
+            n = dp * ns
+            dd = [(d + pos) % world if dp == world else (pos + d * (world // 2)) % world
+                  for d in range(dp) for pos in range(ns)]
+            bp = runner.broadcast_plan(dd, dp)
+            assert [b[0] for b in bp] == list(range(ns))
+            assert all(b[1] == dd[b[0]] and len(b[2]) == dp for b in bp)
+            groups = runner.make_broadcast_groups(dist, bp)
+            bufs = {qq: torch.full((64,), -1.0) for qq in range(n) if dd[qq] == rank}
+            for qq in bufs:
+                if qq < ns:                       # replica 0 holds the synced bytes
+                    bufs[qq] = torch.arange(64, dtype=torch.float32) + 100 * qq
+            runner.run_broadcasts(dist, groups, rank, bufs)
+            for qq, t in bufs.items():
+                assert torch.equal(t, torch.arange(64, dtype=torch.float32) + 100 * (qq % ns)), (dp, ns, qq)
+        with pytest.raises(ValueError):
+            runner.broadcast_plan([0, 0], 2)      # replicas of one position on one GPU
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
