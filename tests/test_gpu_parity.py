@@ -80,6 +80,47 @@ def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("model,fsdp,tpt,tpg,sdt,ddt", [
+    ("toy", 2, 1, 2, "f32", "bf16"),
+    ("toy", 3, 1, 4, "f32", "fp8"),
+    ("toy", 2, 2, 8, "bf16", "mxfp8"),
+    ("toy", 3, 1, 4, "bf16", "mxfp4"),
+    ("toy", 2, 2, 8, "bf16", "nvfp4"),
+    ("ragged", 3, 1, 5, "f32", "bf16"),
+    ("ragged", 7, 5, 1, "bf16", "fp8"),
+    ("wide", 2, 2, 1, "bf16", "mxfp4"),
+])
+def test_guard_bands(rt, model, fsdp, tpt, tpg, sdt, ddt):
+    """Out-of-bounds check without compute-sanitizer (closed on this pool): every
+    trainer and generator buffer sits inside a larger allocation between 64 KiB
+    canary bands; after the sync the generator bytes match the oracle, no canary
+    byte changed (no write before / after any buffer) and the trainer bytes are
+    unchanged (the path only reads them)."""
+    job = _toy_job(rt, model, fsdp, tpt, tpg, sdt, ddt)
+    G = 1 << 16
+    bigs = []
+
+    def guarded(t, canary):
+        big = torch.full((t.numel() + 2 * G,), canary, dtype=torch.uint8, device=t.device)
+        bigs.append((big, t.numel(), canary))
+        return big[G:G + t.numel()]
+
+    job.src = {r: guarded(t, 0xC3) for r, t in job.src.items()}
+    job.dst = {g: guarded(t, 0x3C) for g, t in job.dst.items()}
+    job.src_ptrs = [job.src[r].data_ptr() if r in job.src else 0 for r in range(job.S.n_ranks)]
+    job.dst_ptrs = [job.dst[g].data_ptr() if g in job.dst else 0 for g in range(job.D.n_ranks)]
+    _run_and_compare(rt, job, seed=77)
+    before = {r: t.cpu().numpy().copy() for r, t in job.src.items()}
+    job.sync()
+    torch.cuda.synchronize()
+    for r, t in job.src.items():
+        assert np.array_equal(t.cpu().numpy(), before[r]), f"trainer rank {r} modified"
+    for big, n, canary in bigs:
+        h = big.cpu().numpy()
+        assert (h[:G] == canary).all() and (h[G + n:] == canary).all(), "write outside a rank buffer"
+    job.close()
+
+
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,inner", [
     (2, 1, 2, "f32", "bf16", False),    # C1
     (3, 1, 4, "f32", "fp8", False),     # multi-source (pull) fp8 blocks
