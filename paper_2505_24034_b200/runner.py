@@ -46,7 +46,7 @@ class SyncJob:
     one, the job must fit one device (n_gpus == 1)."""
 
     def __init__(self, spec: JobSpec, device: int | None = None, seed: int = 0, fill: bool = True,
-                 multicast: bool = False, replicate: str = "push"):
+                 multicast: bool = False, replicate: str = "push", double_buffer: bool = False):
         self.spec = spec
         self.cfg = cfg = spec.cfg
         self.model = spec.model()
@@ -97,6 +97,19 @@ class SyncJob:
         self._opened = []
         self.src_ptrs = [self.src[r].data_ptr() if r in self.src else 0 for r in range(self.S.n_ranks)]
         self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else 0 for g in range(self.D.n_ranks)]
+        # NEXT f3: double-buffered generator weights.  `dst` is what the next sync
+        # writes, `front` what the generator reads; swap() exchanges them once a
+        # sync completed, so generation continues during the sync.
+        self.double_buffer = double_buffer
+        self._sets = None
+        self.front = self.dst
+        if double_buffer:
+            if multicast:
+                raise ValueError("double_buffer with multicast is not supported")
+            other = {g: torch.empty_like(t) for g, t in self.dst.items()}
+            optrs = [other[g].data_ptr() if g in other else 0 for g in range(self.D.n_ranks)]
+            self._sets = [(self.dst, self.dst_ptrs), (other, optrs)]
+            self.front = other
         if self.world > 1:
             self._exchange()
             if replicate == "nccl":
@@ -120,6 +133,10 @@ class SyncJob:
                              {r: llrl.ipc_handle(t.data_ptr()) for r, t in self.src.items()},
                              {g: llrl.ipc_handle(t.data_ptr()) for g, t in self.dst.items()
                               if g not in self.mc_ranks})   # multicast buffers are reached via the MC VA
+        extra = None
+        if self._sets is not None:
+            mine["dst1"] = {g: llrl.ipc_handle(t.data_ptr()) for g, t in self._sets[1][0].items()}
+            extra = {"dst1": self._sets[1][1]}
         allm = [None] * self.world
         dist.all_gather_object(allm, mine)
         opened = {}
@@ -129,7 +146,7 @@ class SyncJob:
             opened[handle] = base
             return base
 
-        flags = map_peers(allm, self.device, self.src_ptrs, self.dst_ptrs, opener)
+        flags = map_peers(allm, self.device, self.src_ptrs, self.dst_ptrs, opener, extra)
         for dev, h in flags.items():
             self.comm.import_peer(dev, h)
         self._opened = [(b, 0) for b in opened.values()]
@@ -211,6 +228,18 @@ class SyncJob:
         self.plan.set_multicast(self.device, dst_mc)
         dist.barrier()
 
+    def swap(self):
+        """Double buffering (f3): make the buffers the last sync wrote the generator's
+        front and target the other set with the next sync.  Every process swaps
+        after the same sync (peer pointer sets stay paired); order it after the
+        sync's completion on the generator's stream (the sync's stream, or an
+        event recorded on it)."""
+        if self._sets is None:
+            raise ValueError("swap() needs SyncJob(double_buffer=True)")
+        k = 1 if self.dst is self._sets[0][0] else 0
+        self.front = self.dst
+        self.dst, self.dst_ptrs = self._sets[k]
+
     # -- the hot path ----------------------------------------------------------
     def sync(self, stream=None):
         s = stream if stream is not None else self.stream
@@ -277,6 +306,8 @@ class SyncJob:
             self.comm = None
         self.plan.close()
         self.dst = {}
+        self.front = {}
+        self._sets = None
         for b in self._mc:
             b.close()
         self._mc = []
@@ -299,7 +330,7 @@ def exchange_meta(device, flag_handle, src_handles, dst_handles):
     return {"dev": device, "flag": flag_handle, "src": dict(src_handles), "dst": dict(dst_handles)}
 
 
-def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener):
+def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener, extra=None):
     """Fill src_ptrs / dst_ptrs (in place) with peer-mapped addresses of every rank
     buffer other processes own.  Each distinct allocation handle is opened once
     (several rank buffers may share one caching-allocator segment); returns
@@ -310,7 +341,8 @@ def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener):
         if m["dev"] == my_device:
             continue
         flags[m["dev"]] = m["flag"]
-        for table, ptrs in (("src", src_ptrs), ("dst", dst_ptrs)):
+        tables = [("src", src_ptrs), ("dst", dst_ptrs)] + list((extra or {}).items())
+        for table, ptrs in tables:
             for r, (h, off) in m[table].items():
                 if h not in bases:
                     bases[h] = opener(h)

@@ -123,6 +123,39 @@ def nccl_replica_case(runner, world, fsdp, tpt, tpg, sdt, ddt, dp, seed=21):
     job.close()
 
 
+def double_buffer_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, seed=31):
+    """f3 across GPUs: peers push into the back set (both sets IPC-mapped), the
+    front set is untouched until every process swaps."""
+    cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, placement)
+    job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False, double_buffer=True)
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, False)
+    for t in list(job.front.values()) + list(job.dst.values()):
+        t.fill_(0x5A)
+    old = harness.oracle_dst(ol, harness.host_src(ol, seed - 1), 0x5A)
+    first = True
+    for rep in range(3):
+        src = harness.host_src(ol, seed + rep)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        torch.cuda.synchronize()
+        snap = {g: t.cpu().numpy().copy() for g, t in job.front.items()}
+        dist.barrier()
+        job.sync()
+        torch.cuda.synchronize()
+        dist.barrier()
+        for g, t in job.front.items():
+            assert np.array_equal(t.cpu().numpy(), snap[g]), f"{cfg} rep {rep}: front rank {g} written"
+            if not first:
+                assert np.array_equal(snap[g], old[g])
+        job.swap()
+        first = False
+        want = harness.oracle_dst(ol, src, 0x5A)
+        for g, t in job.front.items():
+            assert np.array_equal(t.cpu().numpy(), want[g]), f"{cfg} rep {rep}: dst rank {g}"
+        old = want
+    job.close()
+
+
 def full_case(runner, world, name):
     from tests.test_gpu_parity import _sampled_check
     spec = runner.spec_for(name, world)
@@ -176,6 +209,8 @@ def main():
     toy_case(runner, world, world, 1, 1, "f32", "bf16", "colocated", dp=world, multicast=True)
     toy_case(runner, world, 3, 1, 2, "bf16", "bf16", "colocated", dp=world // 2 if world >= 4 else 2,
              multicast=True)
+    double_buffer_case(runner, world, 2, 1, 2, "f32", "bf16", "disjoint")   # f3 double buffering
+    double_buffer_case(runner, world, 2, 2, 8, "bf16", "fp8", "rotated")
     nccl_replica_case(runner, world, 2, 1, 1, "f32", "bf16", world)       # a5 NCCL replication
     nccl_replica_case(runner, world, 2, 2, 2, "bf16", "fp8", world)
     if rank0():

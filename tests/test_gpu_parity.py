@@ -80,6 +80,46 @@ def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", [
+    (2, 1, 2, "f32", "bf16"), (2, 2, 8, "bf16", "fp8"), (3, 1, 4, "bf16", "nvfp4")])
+def test_double_buffered_generator(rt, fsdp, tpt, tpg, sdt, ddt):
+    """NEXT f3: with double buffering the sync writes the back set while the
+    generator's front set stays untouched (a reader on another stream sees the
+    previous weights throughout), and swap() publishes the new weights."""
+    llrl, runner = rt
+    cfg = LayoutConfig("t", "toy", fsdp, tpt, tpg, sdt, ddt, "colocated")
+    job = runner.SyncJob(runner.JobSpec(cfg, 1), fill=False, double_buffer=True)
+    ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, False)
+    for t in list(job.front.values()) + list(job.dst.values()):
+        t.fill_(0x5A)
+    reader = torch.cuda.Stream()
+    prev = None
+    for k in range(3):
+        src = harness.host_src(ol, 40 + k)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        torch.cuda.synchronize()
+        snap = {g: t.clone() for g, t in job.front.items()}
+        reads = []
+        with torch.cuda.stream(reader):           # the "generator" keeps reading its weights
+            for _ in range(4):
+                reads.append({g: t.clone() for g, t in job.front.items()})
+        job.sync()
+        torch.cuda.synchronize()
+        for g, t in job.front.items():            # untouched by the sync
+            assert torch.equal(t, snap[g]), f"sync {k} wrote the front buffer of rank {g}"
+            assert all(torch.equal(rd[g], snap[g]) for rd in reads)
+        job.swap()
+        want = harness.oracle_dst(ol, src, 0x5A)
+        for g, t in job.front.items():
+            assert np.array_equal(t.cpu().numpy(), want[g]), f"sync {k}: front rank {g}"
+        if prev is not None:
+            for g in job.dst:                     # the next target is the older set
+                assert job.dst[g].data_ptr() == prev[g]
+        prev = {g: t.data_ptr() for g, t in job.front.items()}
+    job.close()
+
+
 @pytest.mark.parametrize("model,fsdp,tpt,tpg,sdt,ddt", [
     ("toy", 2, 1, 2, "f32", "bf16"),
     ("toy", 3, 1, 4, "f32", "fp8"),

@@ -65,13 +65,17 @@ def _worker(rank, world, port, q):
                 opened.append(h)
                 return 10 ** 9 * (int(h.decode()[1:]) + 1)
 
-            flags = runner.map_peers(allm, rank, src_ptrs, dst_ptrs, opener)
+            for m in allm:                       # a second generator set (double buffering, f3)
+                m["dst1"] = {g: (h, off + 500) for g, (h, off) in m["dst"].items()}
+            dst1 = [0] * D.n_ranks
+            flags = runner.map_peers(allm, rank, src_ptrs, dst_ptrs, opener, {"dst1": dst1})
             assert sorted(opened) == sorted({f"h{p}".encode() for p in range(world) if p != rank})
             assert set(flags) == {p for p in range(world) if p != rank}
             assert all(src_ptrs) and all(dst_ptrs)
             for g in range(D.n_ranks):
                 if dd[g] != rank:
                     assert dst_ptrs[g] == 10 ** 9 * (dd[g] + 1) + 5000 + 1000 * g
+                    assert dst1[g] == dst_ptrs[g] + 500
         # a5 NCCL-style replica broadcast (runner.broadcast_plan / run_broadcasts) on gloo:
         # replica 0's buffers reach every replica, other ranks' buffers stay untouched
         import torch
