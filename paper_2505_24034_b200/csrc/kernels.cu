@@ -601,7 +601,13 @@ __device__ __forceinline__ int cast_chunks(const Item &it, int es, int *rows_per
 template <int SB>
 __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per, int segs_per_row, int k) {
     Chunk c;
-    if (segs_per_row == 1) {
+    if (it.rows == 1) {                 // one (long) row: segments, no division
+        const int seg_elems = SB / es;
+        c.r0 = 0;
+        c.nr = 1;
+        c.c0 = k * seg_elems;
+        c.nc = min(seg_elems, it.cols - c.c0);
+    } else if (segs_per_row == 1) {
         c.r0 = k * rows_per;
         c.nr = min(rows_per, it.rows - c.r0);
         c.c0 = 0;
@@ -794,10 +800,12 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                         // NVFP4 (R16): each thread's 16 elements are one 1x16 group
                         const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
                         // NVFP4 scale byte of unit u: nv_s0 + u, plus nv_gap per chunk row
-                        const int64_t nv_s0 = it.aux + (it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) / kNvGroup;
-                        const int nv_gap = c.nr > 1 ? int((it.dst_ld - c.nc) / kNvGroup) : 0;
-                        const int64_t mx_s0 = it.aux + (it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) / kMxGroup;
-                        const int mx_gap = c.nr > 1 ? int((it.dst_ld - c.nc) / kMxGroup) : 0;
+                        // (the row of unit u is floor((u + 0.5) / upr) through a float reciprocal:
+                        // exact for upr <= 1024 units per chunk row, error < 2^-12)
+                        const int gsh = nv ? 4 : 5;                  // log2 of the group size (offsets >= 0)
+                        char *sb = dbase + it.aux + ((it.dst_off + int64_t(c.r0) * it.dst_ld + c.c0) >> gsh);
+                        const int gap = c.nr > 1 ? int((it.dst_ld - c.nc) >> gsh) : 0;
+                        const float inv_upr = __frcp_rn(float(c.nc / 16));
                         for (int u0 = 0; u0 < nunits; u0 += kCastWorkers) {
                             const int u = u0 + wt;
                             const bool live = u < nunits;
@@ -820,10 +828,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                 const float r = nv_r[nv_buf][sc];
                                 if (live) {
                                     reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, r);
-                                    // group index: dst_off, dst_ld and c0 are multiples of 16
-                                    int64_t g = nv_s0 + u;
-                                    if (nv_gap) g += int64_t(u / (c.nc / kNvGroup)) * nv_gap;
-                                    dbase[g] = static_cast<char>(sc);
+                                    // scale byte: sb[u], plus gap per chunk row (dst_off, dst_ld, c0: whole groups)
+                                    int g = u;
+                                    if (gap) g += __float2int_rz((float(u) + 0.5f) * inv_upr) * gap;
+                                    sb[g] = static_cast<char>(sc);
                                 }
                                 continue;
                             }
@@ -836,9 +844,9 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                 if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
                                 else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
                                 if ((u & 1) == 0) {   // group index as for NVFP4, 32-element groups
-                                    int64_t g = mx_s0 + (u >> 1);
-                                    if (mx_gap) g += int64_t(u / (c.nc / 16)) * mx_gap;
-                                    dbase[g] = static_cast<char>(code);
+                                    int g = u >> 1;
+                                    if (gap) g += __float2int_rz((float(u) + 0.5f) * inv_upr) * gap;
+                                    sb[g] = static_cast<char>(code);
                                 }
                             }
                         }
