@@ -580,6 +580,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_
 // TMA cast kernel configurations: (stage bytes, stages, worker threads, CTAs/SM)
 #define LLRL_TMA_A 32 * 1024, 4, 512, 1
 #define LLRL_TMA_B 16 * 1024, 4, 256, 2
+#define LLRL_TMA_C 32 * 1024, 4, 256, 1
 
 // Chunk k of a cast item: `nr` rows x `nc` columns starting at (r0, c0) of the
 // item, at most kCastStageBytes of source.  Same enumeration on both roles.
@@ -1054,6 +1055,8 @@ static const void *kernel_for(int mode, int variant, bool src_f32) {
         return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_A> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_A>;
     if (mode == 0 && variant == kCastTmaVariant + 1)
         return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_B> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_B>;
+    if (mode == 0 && variant == kCastTmaVariant + 2)
+        return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_C> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_C>;
     if (mode == 1) {
         if (variant == 0) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
         return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false>;
@@ -1074,6 +1077,10 @@ static void launch_shape(int mode, int variant, bool src_f32, int *threads, size
     if (mode == 0 && variant == kCastTmaVariant + 1) {
         *threads = 64 + 256;
         *smem = size_t(4) * (16 * 1024 + 8 * 1024);
+    }
+    if (mode == 0 && variant == kCastTmaVariant + 2) {
+        *threads = 64 + 256;
+        *smem = size_t(4) * (32 * 1024 + 16 * 1024);
     }
     if (mode == 1 && variant != 0) {
         *threads = kThreads + 32;
@@ -1137,6 +1144,6 @@ cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, threads, smem);
 }
 
-int num_cast_variants() { return kNumCastVariants + 2; }   // + the two TMA variants
+int num_cast_variants() { return kNumCastVariants + 3; }   // + the three TMA variants
 
 }  // namespace llrl

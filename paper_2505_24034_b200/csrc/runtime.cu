@@ -90,10 +90,16 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     // Cast kernel: TMA-staged (G->S->G bulk copies, local or peer) by default --
     // with its dedicated storer warp it matched or beat the register kernel on
     // every HBM- and NVLink-bound config measured (profiles/r01_y_bench_*).
-    W.variant = kDefaultCastVariant;
-    if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
+    // Quantising plans (MX / NVFP4) take the 16 KiB-stage variant with two CTAs
+    // per SM: their workers are instruction-bound and the second CTA hides the
+    // per-chunk setup (C7/C10/C11: 2-3% faster, profiles/r01_var_*); plain
+    // casts keep one CTA with 32 KiB stages (C2: 2.5% faster).
+    bool has_mx = false;
     for (const Item &it : W.items)
-        if (it.flags & F_MX) { W.variant = kCastTmaVariant; break; }        // MXFP8 lives in the TMA kernel only
+        if (it.flags & F_MX) { has_mx = true; break; }
+    W.variant = has_mx ? kCastTmaVariant + 1 : kDefaultCastVariant;
+    if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
+    if (has_mx && W.variant < kCastTmaVariant) W.variant = kCastTmaVariant + 1;   // MX: TMA kernels only
     if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline

@@ -394,7 +394,7 @@ def test_full_c3_70b_bf16_sampled(rt):
     job.close()
 
 
-@pytest.mark.parametrize("variant", range(8))
+@pytest.mark.parametrize("variant", range(9))
 def test_toy_parity_cast_variants(rt, variant, monkeypatch):
     """Every cast-kernel variant (LLRL_CAST_VARIANT tuning knob) is bit-exact."""
     monkeypatch.setenv("LLRL_CAST_VARIANT", str(variant))
