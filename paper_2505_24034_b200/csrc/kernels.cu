@@ -3,7 +3,8 @@
 // K1  llrl_k_cast_tma  relayout + cast + move (a3; §5.2: each
 //                      GPU sends its own shards straight into the generator's
 //                      CUDA memory over NVLink, no CPU, no PS hop), plus the
-//                      MXFP8 / MXFP4 row-group quantisation (R13, R15).
+//                      MXFP8 / MXFP4 / NVFP4 row-group quantisation (R13, R15,
+//                      R16).
 //                      Warp-specialised: a producer warp stages rows with
 //                      cp.async.bulk (TMA) into a 4-deep shared-memory ring,
 //                      worker warps convert in shared memory, a storer warp
@@ -16,11 +17,13 @@
 // K3  completion       (a6): last CTA of a launch publishes a release add to every
 //                      destination GPU's per-sender counter; llrl_k_wait spins
 //                      with acquire loads (R10).
+// K4  llrl_k_nv_amax   NVFP4 per-tensor partial amax (bulk-copy staged), the
+// K5  llrl_k_nv_scale / llrl_k_nv_fetch  cross-GPU amax handshake (R16).
 //
 // The work is memory movement with about one ALU op per element: no dense
 // contraction, no tensor cores; the design targets HBM and NVLink bandwidth.
-// Every launch is a persistent grid (one CTA per SM for the TMA kernels)
-// striding over work items the planner interleaved across destinations.
+// Every launch is a persistent grid (one or two CTAs per SM for the TMA
+// kernels) striding over work items the planner interleaved across destinations.
 #include <cuda_runtime.h>
 #include <cstdint>
 
