@@ -10,7 +10,8 @@
   on random and special blocks.
 * layout + whole sync: independent brute force (torch.chunk / torch.cat /
   ml_dtypes) over the 80-combination toy sweep and odd layouts; closed-form
-  provenance; dst coverage exactly once; error codes.
+  provenance; dst coverage exactly once; generator shards concatenate back to
+  cast(full) (round trip with an f32 generator); error codes.
 * parameter counts: the public Llama-3.1 sizes (tests/golden/param_counts.txt).
 """
 from __future__ import annotations
@@ -409,3 +410,76 @@ def test_param_counts_match_public_llama_sizes(oracle_lib):
         L = oracle.Layout(MODELS[name], 1, 1, 1)
         total = sum(L.src_param_info(p)[0] * L.src_param_info(p)[1] for p in range(L.n_src_params))
         assert total == int(count), name
+
+
+# --------------------------------------------------------------------------- invariants (SURVEY §8(c) pins iii)
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", [
+    (2, 1, 4, "f32", "bf16"),      # KV replication (tp_gen 4 > KV 2)
+    (3, 2, 2, "bf16", "bf16"),
+    (4, 1, 1, "f32", "f32"),       # identity: round trip trainer -> generator -> full
+    (2, 2, 8, "f32", "f32"),
+    (1, 1, 8, "bf16", "bf16"),
+])
+def test_oracle_generator_shards_concatenate_to_cast_full(oracle_lib, fsdp, tpt, tpg, sdt, ddt):
+    """Un-fusing every generator rank's qkv / gate_up and concatenating the shards
+    along the split dimension gives cast(full(p)) for every parameter; norms are
+    full copies on every rank; with tp_gen > KV each rank's k / v is its head
+    group's slice.  With an f32 generator this is the round trip
+    trainer shards -> generator shards -> the full tensor the trainer shards were
+    cut from.  Independent of brute.py's per-rank slicing: here the full tensors
+    are rebuilt from the oracle's output."""
+    m = MODELS["toy"]
+    seed = 23
+    ol = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt)
+    dst = harness_oracle_dst(ol, seed)
+    full = brute.full_tensors(m, seed, sdt)
+    if ddt == "bf16" and sdt == "f32":
+        cast = {k: v.view(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16) for k, v in full.items()}
+    else:
+        cast = full
+    odt = np.uint16 if ddt == "bf16" else np.uint32
+    es = np.dtype(odt).itemsize
+
+    def tensor(g, gp):
+        R, C, q, off, _ = ol.dst_param(g, gp)
+        assert q == 0
+        return dst[g][off:off + R * C * es].view(odt).reshape(R, C)
+
+    H, KV, hd = m.n_heads, m.n_kv_heads, m.head_dim
+    qr = H * hd // tpg
+    kvr = hd if tpg > KV else KV * hd // tpg
+    gps = ["embed"] + [f"l{l}.{n}" for l in range(m.n_layers)
+                       for n in ("attn_norm", "qkv", "o", "mlp_norm", "gate_up", "down")] + ["final_norm", "lm_head"]
+    assert len(gps) == ol.n_dst_params
+    for gp, name in enumerate(gps):
+        shards = [tensor(g, gp) for g in range(tpg)]
+        base = name.split(".")[-1]
+        pre = name[:-len(base)]
+        if base in ("attn_norm", "mlp_norm", "final_norm"):
+            for s in shards:
+                assert np.array_equal(s.reshape(-1), cast[name].reshape(-1)), name
+        elif base in ("embed", "lm_head"):
+            assert np.array_equal(np.concatenate(shards, 0), cast[name]), name
+        elif base in ("o", "down"):
+            assert np.array_equal(np.concatenate(shards, 1), cast[name]), name
+        elif base == "gate_up":
+            f = m.d_ffn // tpg
+            assert np.array_equal(np.concatenate([s[:f] for s in shards], 0), cast[pre + "gate"]), name
+            assert np.array_equal(np.concatenate([s[f:] for s in shards], 0), cast[pre + "up"]), name
+        else:                                   # qkv
+            assert np.array_equal(np.concatenate([s[:qr] for s in shards], 0), cast[pre + "q"]), name
+            for j, kv in enumerate(("k", "v")):
+                parts = [s[qr + j * kvr:qr + (j + 1) * kvr] for s in shards]
+                if tpg > KV:                    # rank g holds head g // (tpg / KV)
+                    rep = tpg // KV
+                    for g in range(tpg):
+                        h = g // rep
+                        assert np.array_equal(parts[g], cast[pre + kv][h * hd:(h + 1) * hd]), (name, kv, g)
+                    parts = parts[::rep]
+                assert np.array_equal(np.concatenate(parts, 0), cast[pre + kv]), (name, kv)
+
+
+def harness_oracle_dst(ol, seed):
+    from tests import harness
+    return harness.oracle_dst(ol, harness.host_src(ol, seed))
