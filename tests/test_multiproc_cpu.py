@@ -1,4 +1,4 @@
-"""N>1 host logic on CPU with world_size-2 gloo process groups: every rank
+"""N>1 host logic on CPU with world_size-2, -4 and -8 gloo process groups: every rank
 builds the same plan independently, the per-device shares add up to the whole
 sync, each device's expected arrivals match the senders that signal it, and
 the IPC exchange (runner.map_peers) maps every peer buffer a device's work
@@ -104,7 +104,7 @@ def _worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_multiprocess_plan_and_exchange_gloo(world):
     from paper_2505_24034_b200 import build
     build.build()
