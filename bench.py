@@ -335,6 +335,9 @@ def run_llrl(args):
                        "multicast": bool(args.multicast and job.mc_positions()[0]),
                        "replicate": args.replicate,
                        "timing": "isolated syncs (barrier before each)" if args.step_sync else "back-to-back syncs",
+                       "regime": ("all ranks on one GPU: local HBM re-layout + cast" if args.gpus == 1 else
+                                  f"{cfg.placement} placement over {args.gpus} GPUs: fused pushes over NVLink"
+                                  " (G=1 and G>=2 are different regimes; compare each to roofline.t_lb_ms)"),
                        "n_layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
                        "l2": "inputs >> 126 MB L2 (no flush needed)"},
