@@ -222,6 +222,7 @@ struct llrl_plan {
     std::vector<int> src_device, dst_device;
     std::vector<int64_t> src_rank_bytes, dst_rank_bytes;
     int n_groups = 0;
+    bool model_with_embed = false;       // groups: 0 = embed, 1..L = layers, L+1 = final_norm + lm_head
     std::vector<std::vector<std::pair<int64_t, int64_t>>> src_group_range, dst_group_range;   // [rank][group]
     std::vector<llrl::Tile> tiles;
     std::vector<llrl::DeviceWork> dev;   // indexed by device ordinal

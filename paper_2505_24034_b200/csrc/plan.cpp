@@ -297,6 +297,7 @@ struct Builder {
         const int G = P->n_devices;
         n_groups = S->model.n_layers + (S->model.with_embed ? 2 : 0);
         P->n_groups = n_groups;
+        P->model_with_embed = S->model.with_embed != 0;
         lists.assign(G, std::vector<std::vector<std::vector<Item>>>(G, std::vector<std::vector<Item>>(n_groups)));
         mc_extra.assign(size_t(G), std::vector<std::vector<int>>(size_t(n_groups)));
         seglists.assign(G, {});

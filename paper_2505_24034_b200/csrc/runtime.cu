@@ -455,7 +455,23 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
     CK(cudaEventRecord(ev(size_t(2 * G)), s));
     CK(cudaStreamWaitEvent(h2d, ev(size_t(2 * G)), 0));
     CK(cudaStreamWaitEvent(d2h, ev(size_t(2 * G)), 0));
-    for (int g = 0; g < G; g++) {
+    // Group order: the first group's H2D and the last group's D2H are not
+    // overlapped with anything, so the (large) embedding and lm_head groups go
+    // to the middle of the pipeline and decoder layers open and close it.  Every
+    // device uses the same order (per-sender arrival counts stay paired).
+    std::vector<int> order;
+    if (p->model_with_embed && G >= 4) {
+        for (int g = 1; g < G - 1; g++) {
+            order.push_back(g);
+            if (g == G / 2) {
+                order.push_back(0);
+                order.push_back(G - 1);
+            }
+        }
+    } else {
+        for (int g = 0; g < G; g++) order.push_back(g);
+    }
+    for (int g : order) {
         for (int r = 0; r < p->n_src; r++) {
             const auto &rg = p->src_group_range[size_t(r)][size_t(g)];
             if (p->src_device[size_t(r)] != device || !host_src[r] || rg.first < 0) continue;
