@@ -297,6 +297,9 @@ def run_llrl(args):
     roof = {"bound": res, "achieved": round(nbytes / ms / 1e6, 1), "peak": peak, "unit": "GB/s",
             "peak_source": peak_src if res == "hbm" else "measured peer copy per direction (B200_PROFILING.md)"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    nominal = 8000.0 if res == "hbm" else 900.0                      # B200 HBM3e / NVLink 5 per direction
+    roof["frac_nominal"] = round(roof["achieved"] / nominal, 4)
+    roof["nominal_peak"] = nominal
     roof["traffic"] = _ncu_traffic(args.config, args.gpus)
     info = job.plan.device_info(bdev)
     kern = []
