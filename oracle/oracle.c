@@ -421,14 +421,6 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (c->fsdp <= 0 || c->tp_train <= 0 || c->tp_gen <= 0 || c->dp_gen <= 0 ||
         c->pp_train <= 0 || c->pp_gen <= 0)
         return ORC_E_INVALID;
-    /* R15: MXFP4 packs two elements per byte: every quantised generator tensor has
-     * an even number of columns (and, for whole 1x32 groups, a multiple of 32) */
-    if (c->dst_dtype == ORC_MXFP4 && (m->d_model % 32 || (m->n_heads * m->head_dim / c->tp_gen) % 32 ||
-                                      (m->d_ffn / c->tp_gen) % 32))
-        return ORC_E_UNSUPPORTED;
-    if (c->dst_dtype == ORC_NVFP4 && (m->d_model % 16 || (m->n_heads * m->head_dim / c->tp_gen) % 16 ||
-                                      (m->d_ffn / c->tp_gen) % 16))
-        return ORC_E_UNSUPPORTED;
     /* R14: whole layers per stage */
     if (m->n_layers % c->pp_train || m->n_layers % c->pp_gen)
         return ORC_E_INDIVISIBLE;
@@ -452,6 +444,16 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (m->n_kv_heads % T && T % m->n_kv_heads) return ORC_E_INDIVISIBLE;
     if (m->d_ffn % T) return ORC_E_INDIVISIBLE;
     if (m->with_embed && m->vocab % T) return ORC_E_INDIVISIBLE;
+    /* R15: MXFP4 packs two elements per byte: every quantised generator tensor has
+     * an even number of columns (and, for whole 1x32 groups, a multiple of 32);
+     * R16 likewise with 1x16 groups.  Checked after the divisibility rules (a
+     * layout that violates both reports INDIVISIBLE, as the library does). */
+    if (c->dst_dtype == ORC_MXFP4 && (m->d_model % 32 || (m->n_heads * m->head_dim / c->tp_gen) % 32 ||
+                                      (m->d_ffn / c->tp_gen) % 32))
+        return ORC_E_UNSUPPORTED;
+    if (c->dst_dtype == ORC_NVFP4 && (m->d_model % 16 || (m->n_heads * m->head_dim / c->tp_gen) % 16 ||
+                                      (m->d_ffn / c->tp_gen) % 16))
+        return ORC_E_UNSUPPORTED;
     return ORC_OK;
 }
 
