@@ -156,6 +156,71 @@ def double_buffer_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, seed=
     job.close()
 
 
+def random_cases(runner, world, n=16, seed=2505):
+    """Seeded random shapes and layouts (the same draws on every rank), each
+    through llrl_sync across the GPUs twice and compared with the oracle byte
+    for byte; invalid draws are skipped the same way on every rank."""
+    from synth import MODELS
+    from synth.configs import Model
+    rng = np.random.default_rng(seed)
+    ran = 0
+    for i in range(400):
+        if ran >= n:
+            break
+        ddt_s = [("f32", "bf16"), ("bf16", "bf16"), ("f32", "f32"), ("bf16", "fp8"), ("f32", "fp8"),
+                 ("bf16", "mxfp8"), ("f32", "mxfp4"), ("bf16", "nvfp4")]
+        sdt, ddt = ddt_s[rng.integers(len(ddt_s))]
+        tpt = int(rng.choice([1, 2, 3, 4]))
+        tpg = int(rng.choice([1, 2, 4, 8]))
+        unit = tpt * tpg // int(np.gcd(tpt, tpg))
+        if ddt in ("mxfp8", "mxfp4", "nvfp4"):
+            unit *= 32
+        kv = int(rng.choice(sorted({1, 2, 4, tpg})))
+        m = Model(int(rng.integers(1, 3)), unit * int(rng.choice([1, 2])) * 8, kv * int(rng.choice([1, 2, unit])),
+                  kv, int(rng.choice([8, 16, 32])), unit * int(rng.choice([8, 12])), unit * int(rng.choice([4, 6])),
+                  int(rng.integers(0, 2)))
+        d, q, k = m.d_model, m.n_heads * m.head_dim, m.n_kv_heads * m.head_dim
+        if m.n_layers * (d * (q + 2 * k) + q * d + 3 * d * m.d_ffn) + 2 * m.vocab * d > 3_000_000:
+            continue
+        fsdp = int(rng.integers(1, 5))
+        inner = bool(rng.integers(0, 2))
+        dp, ppt, ppg = (int(rng.choice([1, 1, 2])) for _ in range(3))
+        placement = str(rng.choice(["colocated", "rotated", "disjoint"]))
+        O = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, inner, dp, ppt, ppg)
+        if O.status != 0:
+            continue
+        name = f"rnd{i}"
+        MODELS[name] = m
+        cfg = LayoutConfig(name, name, fsdp, tpt, tpg, sdt, ddt, placement, inner, dp_gen=dp, pp_train=ppt,
+                           pp_gen=ppg)
+        try:
+            job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False)
+        except Exception as e:           # tiles splitting a 1x32 / 1x16 group: UNSUPPORTED (R13, R16)
+            assert "UNSUPPORTED" in str(e) or "status -4" in str(e), e
+            dist.barrier()
+            continue
+        src = harness.host_src(O, 11 + i)
+        want = harness.oracle_dst(O, src, 0x5A)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x5A)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(2):
+            job.sync()
+        torch.cuda.synchronize()
+        dist.barrier()
+        for g, t in job.dst.items():
+            got = t.cpu().numpy()
+            if not np.array_equal(got, want[g]):
+                bad = np.nonzero(got != want[g])[0]
+                raise AssertionError(f"random case {i} {m} {cfg}: dst rank {g}: {bad.size} bytes, first {bad[:6]}")
+        job.close()
+        ran += 1
+    assert ran >= n // 2, f"only {ran} random cases ran"
+
+
 def full_case(runner, world, name):
     from tests.test_gpu_parity import _sampled_check
     spec = runner.spec_for(name, world)
@@ -211,6 +276,9 @@ def main():
              multicast=True)
     double_buffer_case(runner, world, 2, 1, 2, "f32", "bf16", "disjoint")   # f3 double buffering
     double_buffer_case(runner, world, 2, 2, 8, "bf16", "fp8", "rotated")
+    random_cases(runner, world)                                            # seeded random shapes / layouts
+    if rank0():
+        print("ok random cases", flush=True)
     nccl_replica_case(runner, world, 2, 1, 1, "f32", "bf16", world)       # a5 NCCL replication
     nccl_replica_case(runner, world, 2, 2, 2, "bf16", "fp8", world)
     if rank0():
