@@ -485,6 +485,43 @@ def test_toy_parity_cuda_graph_replay(rt, sdt, ddt):
     job.close()
 
 
+@pytest.mark.parametrize("sdt,f,tt,tg", [("bf16", 2, 2, 8), ("f32", 3, 1, 4)])
+def test_toy_parity_cuda_graph_replay_nvfp4(rt, sdt, f, tt, tg):
+    """NVFP4 sync captured in a CUDA graph: the amax handshake (memset, amax,
+    scale, fetch kernels, waits) and the quantising cast replay with new
+    trainer values each time (tensor amax and scales change)."""
+    job = _toy_job(rt, "toy", f, tt, tg, sdt, "nvfp4")
+    ol = oracle.Layout(job.model, f, tt, tg, sdt, "nvfp4")
+    job.sync()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        job.sync(stream=torch.cuda.current_stream())
+    for rep in range(3):
+        src = harness.host_src(ol, 90 + rep)
+        if rep >= 1:      # halve layer 0's q shard on trainer rank 0: its tensor amax drops,
+            off, r0, r1, c0, c1 = ol.src_piece(0, 2)     # so a stale (not reset) amax would show
+            n = (r1 - r0) * (c1 - c0)
+            if sdt == "f32":
+                x = src[0][off:off + 4 * n].view(np.float32)
+                x *= np.float32(0.5)
+            else:
+                x = src[0][off:off + 2 * n].view(np.uint16)
+                e = (x >> 7) & 0xFF
+                x[e > 1] -= np.uint16(0x80)
+        for r, t in job.src.items():
+            t.copy_(torch.from_numpy(src[r]))
+        for t in job.dst.values():
+            t.fill_(0x3C)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        want = harness.oracle_dst(ol, src, 0x3C)
+        for q, t in job.dst.items():
+            assert np.array_equal(t.cpu().numpy(), want[q]), (rep, q)
+    job.close()
+
+
 @pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8),
                                            ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8)])
 def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
