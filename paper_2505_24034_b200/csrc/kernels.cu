@@ -505,9 +505,9 @@ __host__ __device__ constexpr int fp8_stages() { return SRC_F32 ? 3 : 3; }
 template <bool SRC_F32>
 __host__ __device__ constexpr int fp8_stage_bytes() { return 128 * 128 * (SRC_F32 ? 4 : 2); }
 
-template <bool SRC_F32>
-__global__ void __launch_bounds__(kThreads + 32, 2) llrl_k_fp8_tma(const __grid_constant__ KParams P) {
-    constexpr int S = fp8_stages<SRC_F32>();
+template <bool SRC_F32, int NST = fp8_stages<SRC_F32>(), int MINB = 2>
+__global__ void __launch_bounds__(kThreads + 32, MINB) llrl_k_fp8_tma(const __grid_constant__ KParams P) {
+    constexpr int S = NST;
     constexpr int kStage = fp8_stage_bytes<SRC_F32>();
     constexpr int es = SRC_F32 ? 4 : 2;
     extern __shared__ __align__(128) unsigned char stages[];
@@ -1062,6 +1062,8 @@ static const void *kernel_for(int mode, int variant, bool src_f32) {
         return src_f32 ? (const void *)llrl_k_cast_tma<true, LLRL_TMA_C> : (const void *)llrl_k_cast_tma<false, LLRL_TMA_C>;
     if (mode == 1) {
         if (variant == 0) return src_f32 ? (const void *)llrl_k_fp8<true> : (const void *)llrl_k_fp8<false>;
+        if (variant == 2) return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false, 6, 1>;
+        if (variant == 3) return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false, 2, 3>;
         return src_f32 ? (const void *)llrl_k_fp8_tma<true> : (const void *)llrl_k_fp8_tma<false>;
     }
     if (variant < 0 || variant >= kNumCastVariants)   // out of range: the default TMA variant
@@ -1085,10 +1087,10 @@ static void launch_shape(int mode, int variant, bool src_f32, int *threads, size
         *threads = 64 + 256;
         *smem = size_t(4) * (32 * 1024 + 16 * 1024);
     }
-    if (mode == 1 && variant != 0) {
-        *threads = kThreads + 32;
-        *smem = src_f32 ? size_t(fp8_stages<true>()) * fp8_stage_bytes<true>()
-                        : size_t(fp8_stages<false>()) * fp8_stage_bytes<false>();
+    if (mode == 1 && variant != 0) {   // fp8 TMA variants (bf16 source): 1 = 3 stages x 2 CTAs/SM,
+        *threads = kThreads + 32;      // 2 = 6 stages x 1 CTA/SM, 3 = 2 stages x 3 CTAs/SM
+        const int st = src_f32 ? fp8_stages<true>() : variant == 2 ? 6 : variant == 3 ? 2 : fp8_stages<false>();
+        *smem = size_t(st) * (src_f32 ? fp8_stage_bytes<true>() : fp8_stage_bytes<false>());
     }
 }
 

@@ -103,7 +103,7 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
-    if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = atoi(v) ? 1 : 0;
+    if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = std::min(std::max(atoi(v), 0), 3);
     for (int mode = 0; mode < 2; mode++) {
         int per_sm = 0;
         CK(sync_occupancy(mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, &per_sm));
@@ -233,7 +233,7 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
 static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, KParams &kp, int64_t c0, int64_t c1,
                                  int64_t f0, int64_t f1, const std::vector<int> &sig, cudaStream_t s) {
     const bool has_fp8 = f1 > f0;
-    if (has_fp8 && W.fp8_variant == 1) {
+    if (has_fp8 && W.fp8_variant >= 1) {
         llrl_status st = ensure_tmaps(p, W, const_cast<void *const *>(kp.src), s);
         if (st != LLRL_OK) return st;
     }

@@ -404,7 +404,7 @@ def test_toy_parity_cast_variants(rt, variant, monkeypatch):
         job.close()
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_toy_parity_fp8_variants(rt, variant, monkeypatch):
     """Both fp8 kernels (register / TMA-pipelined, LLRL_FP8_VARIANT) are bit-exact,
     including multi-source (pull) blocks and partial edge blocks."""
