@@ -250,11 +250,13 @@ class SyncJob:
             with torch.cuda.stream(s):
                 run_broadcasts(_dist(), self._bcast, self.device, self.dst)
             return
-        self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+        if self._in_plan():              # a GPU without trainer or generator ranks has no work
+            self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
     def sync_group(self, group, stream=None):
         s = stream if stream is not None else self.stream
-        self.plan.sync_group(self.comm, self.device, group, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+        if self._in_plan():
+            self.plan.sync_group(self.comm, self.device, group, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
     def src_group_views(self, group):
         """Views of this device's trainer bytes of one layer group (for an optimizer step)."""
@@ -286,7 +288,8 @@ class SyncJob:
         s = stream if stream is not None else self.stream
         hs = [host_src[r].data_ptr() if r in host_src else 0 for r in range(self.S.n_ranks)]
         hd = [host_dst[g].data_ptr() if g in host_dst else 0 for g in range(self.D.n_ranks)]
-        self.plan.sync_host(self.comm, self.device, hs, hd, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+        if self._in_plan():
+            self.plan.sync_host(self.comm, self.device, hs, hd, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
 
     def _in_plan(self):
         return self.device in set(self.plan.src_device) | set(self.plan.dst_device)
