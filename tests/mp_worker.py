@@ -156,7 +156,7 @@ def double_buffer_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, seed=
     job.close()
 
 
-def random_cases(runner, world, n=16, seed=2505):
+def random_cases(runner, world, n=24, seed=2505):
     """Seeded random shapes and layouts (the same draws on every rank), each
     through llrl_sync across the GPUs twice and compared with the oracle byte
     for byte; invalid draws are skipped the same way on every rank."""
@@ -216,6 +216,25 @@ def random_cases(runner, world, n=16, seed=2505):
             if not np.array_equal(got, want[g]):
                 bad = np.nonzero(got != want[g])[0]
                 raise AssertionError(f"random case {i} {m} {cfg}: dst rank {g}: {bad.size} bytes, first {bad[:6]}")
+        if ddt != "nvfp4":                 # layer-group streaming and the host-buffer pipeline
+            for t in job.dst.values():
+                t.fill_(0x5A)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for grp in range(job.plan.num_groups()):
+                job.sync_group(grp)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for g, t in job.dst.items():
+                assert np.array_equal(t.cpu().numpy(), want[g]), f"random case {i} {cfg}: sync_group rank {g}"
+            hs = {r: torch.from_numpy(src[r]).pin_memory() for r in job.src}
+            hd = {g: torch.full((job.D.rank_bytes(g),), 0x5A, dtype=torch.uint8).pin_memory() for g in job.dst}
+            dist.barrier()
+            job.sync_host(hs, hd)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for g in job.dst:
+                assert np.array_equal(hd[g].numpy(), want[g]), f"random case {i} {cfg}: sync_host rank {g}"
         job.close()
         ran += 1
     assert ran >= n // 2, f"only {ran} random cases ran"
