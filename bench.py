@@ -134,7 +134,7 @@ def _barrier():
 
 # ---------------------------------------------------------------- CPU oracle legs
 
-def _oracle_sample(cfg_name, seed=0):
+def _oracle_sample(cfg_name, seed=0, stages=1):
     """A bounded sample of the workload for the CPU oracle: one decoder layer per
     pipeline stage of the config's model (no embed / lm_head), same layout parameters.  Returns
     (oracle layout, src buffers, fraction of the full model's elements)."""
@@ -144,7 +144,8 @@ def _oracle_sample(cfg_name, seed=0):
     import math
     cfg = CONFIGS[cfg_name]
     full = MODELS[cfg.model]
-    m = full.replace(n_layers=math.lcm(cfg.pp_train, cfg.pp_gen), with_embed=0)   # whole pipeline stages
+    per = math.lcm(cfg.pp_train, cfg.pp_gen)                                      # whole pipeline stages
+    m = full.replace(n_layers=min(full.n_layers, per * stages), with_embed=0)
     ol = oracle.Layout(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
                        cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
     # cheap deterministic values keyed by (param, global row, col): replicated
@@ -182,8 +183,14 @@ def _time_oracle_once(ol, src):
     return dt
 
 
-def cpu_baseline(cfg_name, full_model_name):
+def cpu_baseline(cfg_name, full_model_name, target_s=12.0):
+    """The oracle on a bounded sample sized for ~10-30 s of host CPU work: one
+    decoder layer calibrates, then enough layers for ~target_s seconds run."""
     ol, src, frac = _oracle_sample(cfg_name)
+    t1 = _time_oracle_once(ol, src)
+    k = max(1, min(64, int(round(target_s / max(t1, 1e-3)))))
+    if k > 1:
+        ol, src, frac = _oracle_sample(cfg_name, stages=k)
     dt = _time_oracle_once(ol, src)
     return {"value": round(dt / frac * 1e3, 3), "unit": "ms", "cores": 1, "kind": "oracle",
             "sample": f"{ol.n_layers_sample} decoder layer(s) of {full_model_name} ({frac * 100:.2f}% of the elements), "
