@@ -248,7 +248,11 @@ llrl_status llrl_ipc_close(void *dev_ptr, int64_t offset);
  * base pointers valid in this process (local or peer/IPC-mapped); entries this
  * device never touches may be NULL.  `comm` may be NULL iff the plan uses one
  * device.  Preconditions (step boundary): no one writes the src
- * buffers or reads the dst buffers during the sync.
+ * buffers or reads the dst buffers during the sync.  Syncs of one plan on one
+ * device are stream-ordered: issue them on one stream (or order the streams),
+ * since a plan's per-device completion counters are reused from sync to sync;
+ * every process issues the same sequence of syncs (per-sender arrival counts).
+ * A device that holds no rank of the plan has nothing to do (INVALID if called).
  * Errors: INVALID, NOPEER (a needed peer flag buffer or pointer missing), CUDA. */
 llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device,
                       void *const *src_ptrs, void *const *dst_ptrs, void *stream);
