@@ -252,7 +252,8 @@ llrl_status llrl_ipc_close(void *dev_ptr, int64_t offset);
  * device are stream-ordered: issue them on one stream (or order the streams),
  * since a plan's per-device completion counters are reused from sync to sync;
  * every process issues the same sequence of syncs (per-sender arrival counts).
- * A device that holds no rank of the plan has nothing to do (INVALID if called).
+ * A device that holds no rank of the plan has nothing to do (the call is a
+ * no-op below the plan's highest device ordinal, INVALID above it).
  * Errors: INVALID, NOPEER (a needed peer flag buffer or pointer missing), CUDA. */
 llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device,
                       void *const *src_ptrs, void *const *dst_ptrs, void *stream);
