@@ -17,7 +17,7 @@
  *   parameters.
  *
  * Every convention the paper leaves open is a numbered DESIGN.md reading
- * (R1..R11); the comments below cite them.  Algorithm order:
+ * (R1..R16); the comments below cite them.  Algorithm order:
  *   1. per layer, materialise each full parameter from all trainer shards,
  *      asserting replicas are bitwise equal and every element is covered;
  *   2. for each generator rank build its local (fused) tensors;
