@@ -98,6 +98,15 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     for (const Item &it : W.items)
         if (it.flags & F_MX) { has_mx = true; break; }
     W.variant = has_mx ? kCastTmaVariant + 1 : kDefaultCastVariant;
+    // Tiny syncs (< 64 MB of cast source on this device, e.g. C1) are latency-bound:
+    // the register kernel starts moving bytes sooner than the TMA pipeline
+    // (C1: 15.4 vs 18.8 us per sync; profiles/r01_final/c1v_*).
+    if (!has_mx) {
+        const int64_t es = p->src_dtype == LLRL_F32 ? 4 : 2;
+        int64_t bytes = 0;
+        for (int64_t i = 0; i < n_cast; i++) bytes += int64_t(W.items[size_t(i)].rows) * W.items[size_t(i)].cols * es;
+        if (bytes < (int64_t(64) << 20)) W.variant = 1;
+    }
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     if (has_mx && W.variant < kCastTmaVariant) W.variant = kCastTmaVariant + 1;   // MX: TMA kernels only
     if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel

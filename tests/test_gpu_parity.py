@@ -28,6 +28,16 @@ def rt():
     return llrl, runner
 
 
+@pytest.fixture(params=["default", "tma"])
+def cast_path(request, monkeypatch):
+    """Toy syncs are tiny, so the product picks the register cast kernel for them
+    (runtime.cu); run the toy cases through the TMA kernel the large syncs use as
+    well."""
+    if request.param == "tma":
+        monkeypatch.setenv("LLRL_CAST_VARIANT", "6")
+    return request.param
+
+
 def _toy_job(rt, model_name, fsdp, tpt, tpg, sdt, ddt, inner=False, n_layers=None, dp=1, ppt=1, ppg=1):
     llrl, runner = rt
     cfg = LayoutConfig("t", model_name, fsdp, tpt, tpg, sdt, ddt, "colocated", inner, dp_gen=dp, pp_train=ppt,
@@ -74,7 +84,7 @@ SWEEP = [(f, tt, tg, sdt, ddt) for f in (1, 2, 3, 8) for tt in (1, 2, 4) for tg 
 
 
 @pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt", SWEEP)
-def test_toy_parity_sweep(rt, fsdp, tpt, tpg, sdt, ddt):
+def test_toy_parity_sweep(rt, cast_path, fsdp, tpt, tpg, sdt, ddt):
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt)
     _run_and_compare(rt, job, seed=fsdp * 100 + tpt * 10 + tpg)
     job.close()
@@ -130,7 +140,7 @@ def test_double_buffered_generator(rt, fsdp, tpt, tpg, sdt, ddt):
     ("ragged", 7, 5, 1, "bf16", "fp8"),
     ("wide", 2, 2, 1, "bf16", "mxfp4"),
 ])
-def test_guard_bands(rt, model, fsdp, tpt, tpg, sdt, ddt):
+def test_guard_bands(rt, cast_path, model, fsdp, tpt, tpg, sdt, ddt):
     """Out-of-bounds check without compute-sanitizer (closed on this pool): every
     trainer and generator buffer sits inside a larger allocation between 64 KiB
     canary bands; after the sync the generator bytes match the oracle, no canary
@@ -176,7 +186,7 @@ def test_guard_bands(rt, model, fsdp, tpt, tpg, sdt, ddt):
     (2, 2, 8, "bf16", "nvfp4", True),
     (3, 1, 4, "bf16", "nvfp4", False),
 ])
-def test_toy_parity_odd(rt, fsdp, tpt, tpg, sdt, ddt, inner):
+def test_toy_parity_odd(rt, cast_path, fsdp, tpt, tpg, sdt, ddt, inner):
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, inner)
     _run_and_compare(rt, job, seed=9)
     job.close()
@@ -205,7 +215,7 @@ def _inject_specials(ol, src):
 @pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("f32", "fp8"), ("bf16", "fp8"), ("bf16", "bf16"),
                                      ("f32", "mxfp8"), ("bf16", "mxfp8"), ("f32", "mxfp4"), ("bf16", "mxfp4"),
                                      ("f32", "nvfp4"), ("bf16", "nvfp4")])
-def test_toy_parity_special_values(rt, sdt, ddt):
+def test_toy_parity_special_values(rt, cast_path, sdt, ddt):
     # tp_train = 1: no replicated trainer pieces, so injected values stay consistent
     job = _toy_job(rt, "toy", 3, 1, 4, sdt, ddt)
     _run_and_compare(rt, job, seed=5, inject=_inject_specials)
@@ -213,7 +223,7 @@ def test_toy_parity_special_values(rt, sdt, ddt):
 
 
 @pytest.mark.parametrize("fsdp,tpt,tpg,dp,sdt,ddt", [(4, 1, 1, 4, "f32", "bf16"), (2, 2, 2, 3, "bf16", "fp8")])
-def test_toy_parity_generator_dp(rt, fsdp, tpt, tpg, dp, sdt, ddt):
+def test_toy_parity_generator_dp(rt, cast_path, fsdp, tpt, tpg, dp, sdt, ddt):
     """Generator DP replicas (R12) filled from the same trainer shards."""
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, dp=dp)
     _run_and_compare(rt, job, seed=13)
@@ -222,7 +232,7 @@ def test_toy_parity_generator_dp(rt, fsdp, tpt, tpg, dp, sdt, ddt):
 
 @pytest.mark.parametrize("fsdp,tpt,ppt,tpg,ppg,dp,sdt,ddt", [
     (2, 1, 2, 2, 1, 1, "f32", "bf16"), (1, 2, 1, 2, 2, 1, "bf16", "fp8"), (3, 1, 2, 4, 2, 2, "f32", "mxfp8")])
-def test_toy_parity_pipeline_stages(rt, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
+def test_toy_parity_pipeline_stages(rt, cast_path, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
     """Decoupled pipeline parallelism (R14), with and without DP replicas."""
     job = _toy_job(rt, "toy", fsdp, tpt, tpg, sdt, ddt, dp=dp, ppt=ppt, ppg=ppg)
     _run_and_compare(rt, job, seed=17)
@@ -234,7 +244,7 @@ def test_toy_parity_pipeline_stages(rt, fsdp, tpt, ppt, tpg, ppg, dp, sdt, ddt):
     ("ragged", 3, 1, 5, "bf16", "fp8"),
     ("wide", 2, 2, 1, "f32", "bf16"), ("wide", 3, 1, 2, "bf16", "fp8"), ("wide", 1, 2, 1, "f32", "mxfp8"),
     ("wide", 2, 2, 1, "bf16", "mxfp4"), ("head_only", 3, 2, 4, "f32", "bf16"), ("toy", 32, 1, 2, "f32", "bf16")])
-def test_edge_shapes_parity(rt, model, fsdp, tpt, tpg, sdt, ddt):
+def test_edge_shapes_parity(rt, cast_path, model, fsdp, tpt, tpg, sdt, ddt):
     """Scalar fallbacks (no dimension a multiple of 8), partial fp8 blocks,
     rows wider than a TMA stage, a model without decoder layers, and trainer
     ranks holding nothing (FSDP 32 over 8-row norms)."""
