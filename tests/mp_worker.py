@@ -281,10 +281,19 @@ def main():
         (2, 2, 8, "bf16", "nvfp4", "colocated"),     # per-tensor amax reduced across GPUs
         (4, 1, 2, "f32", "nvfp4", "disjoint"),
     ]
-    for c in cases:
-        toy_case(runner, world, *c)
-        if dist.get_rank() == 0:
-            print("ok", c, flush=True)
+    # toy syncs are tiny (the product picks the register cast kernel for them):
+    # run them through the TMA kernel of the large syncs as well
+    for path in ("default", "6"):
+        if path == "default":
+            os.environ.pop("LLRL_CAST_VARIANT", None)
+        else:
+            os.environ["LLRL_CAST_VARIANT"] = path
+        for c in cases:
+            toy_case(runner, world, *c)
+            if dist.get_rank() == 0:
+                print("ok", path, c, flush=True)
+        random_cases(runner, world, n=12 if path == "6" else 24, seed=2505 if path == "default" else 77)
+    os.environ.pop("LLRL_CAST_VARIANT", None)
     toy_case(runner, world, 4, 1, 1, "f32", "bf16", "disjoint", dp=4)      # generator DP replicas
     toy_case(runner, world, 2, 2, 2, "bf16", "fp8", "disjoint", dp=2)
     toy_case(runner, world, 2, 2, 8, "bf16", "bf16", "colocated", ppt=2)       # pipeline re-staging
@@ -295,9 +304,6 @@ def main():
              multicast=True)
     double_buffer_case(runner, world, 2, 1, 2, "f32", "bf16", "disjoint")   # f3 double buffering
     double_buffer_case(runner, world, 2, 2, 8, "bf16", "fp8", "rotated")
-    random_cases(runner, world)                                            # seeded random shapes / layouts
-    if rank0():
-        print("ok random cases", flush=True)
     nccl_replica_case(runner, world, 2, 1, 1, "f32", "bf16", world)       # a5 NCCL replication
     nccl_replica_case(runner, world, 2, 2, 2, "bf16", "fp8", world)
     if rank0():
