@@ -205,6 +205,7 @@ struct DeviceWork {
     std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8
     int grid_cast = 0, grid_fp8 = 0;
+    bool no_pdl = false;               // LLRL_PDL=0: plain stream order between the launches
     int variant = 0;                   // cast-kernel variant (kernels.cu)
     int max_ctas = 0;                  // grid cap (0 = all SMs); llrl_plan_set_max_ctas
     int fp8_variant = 1;               // 0: register kernel, 1: TMA pipeline

@@ -419,7 +419,15 @@ __device__ void fp8_item_generic(const Item &it, const KParams &P, uint32_t *s_r
 // destination device with a release add at system scope.  No per-call host
 // state: the launch parameters are the same on every call, so a sync can be
 // captured once in a CUDA graph and replayed.
+// Programmatic dependent launch: a cast launch lets the fp8 launch queued
+// behind it start at once (the two touch disjoint items); the fp8 grid then
+// waits for the cast grid's completion before it completes or signals.
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void complete(const KParams &P) {
+    if (P.pdl_wait) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     if (P.done == nullptr) return;
     __threadfence_system();
     __syncthreads();
@@ -437,6 +445,7 @@ __device__ __forceinline__ void complete(const KParams &P) {
 // K1 launch: relayout + cast items [item_begin, item_end), persistent CTAs.
 template <bool SRC_F32, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) llrl_k_cast(const __grid_constant__ KParams P) {
+    pdl_release();
     for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
         const Item it = P.items[i];
         cast_item<SRC_F32, U>(it, P);
@@ -639,6 +648,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 template <bool SRC_F32, int SB, int NST, int NWK, int MINB>
 __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_constant__ KParams P) {
     constexpr int kCastStageBytes = SB, kCastStages = NST, kCastWorkers = NWK;
+    pdl_release();
     // warp 0: producer (bulk loads global -> shared), warp 1: storer (bulk stores
     // shared -> global), warps 2..: workers (conversion in shared memory).  A stage
     // moves full (producer -> workers) -> converted (workers -> storer) -> empty
@@ -1105,7 +1115,18 @@ cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, i
     size_t smem;
     launch_shape(mode, variant, src_f32, &threads, &smem);
     void *args[] = {const_cast<KParams *>(&P)};
-    return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
+    if (!P.pdl_wait) return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_nv_amax(const NvAmaxParams &P, bool src_f32, int grid, cudaStream_t stream) {

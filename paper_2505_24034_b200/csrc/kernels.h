@@ -24,6 +24,8 @@ struct KParams {
     const void *src[kMaxRanks];
     void *dst[kMaxRanks];
     void *dst_mc[kMaxRanks];           // multicast VA per dst rank (F_MC items)
+    int pdl_wait;                      // launched as a programmatic dependent of the previous
+                                       // launch: wait for it before completing / signalling
 };
 
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)

@@ -112,6 +112,7 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
+    if (const char *v = getenv("LLRL_PDL")) W.no_pdl = atoi(v) == 0;
     if (const char *v = getenv("LLRL_FP8_VARIANT")) W.fp8_variant = std::min(std::max(atoi(v), 0), 3);
     for (int mode = 0; mode < 2; mode++) {
         int per_sm = 0;
@@ -260,7 +261,9 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
             kp.n_signal = int(sig.size());
             for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]] + comm->device;
         }
+        kp.pdl_wait = (mode == 1 && c1 > c0 && !W.no_pdl) ? 1 : 0;   // fp8 launch overlaps the cast tail
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
+        kp.pdl_wait = 0;
     }
     return LLRL_OK;
 }
