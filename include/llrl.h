@@ -59,7 +59,9 @@ typedef enum {
 /* LLRL_NVFP4: E2M1 elements (packed like MXFP4) with one E4M3 scale per 1x16
  * row group and one fp32 scale per generator tensor (reading R16); the tensor
  * scale needs the tensor's global amax, a cross-GPU max-reduction inside the
- * sync (llrl_sync only; llrl_sync_group / llrl_sync_host return UNSUPPORTED). */
+ * sync (llrl_sync_group returns UNSUPPORTED -- a layer group never holds whole
+ * tensors' contributions; llrl_sync_host copies whole buffers in, runs the whole
+ * sync, copies whole buffers out, without per-group pipelining). */
 typedef enum { LLRL_F32 = 0, LLRL_BF16 = 1, LLRL_FP8_E4M3 = 2, LLRL_MXFP8 = 3, LLRL_MXFP4 = 4,
                LLRL_NVFP4 = 5 } llrl_dtype;
 
@@ -278,8 +280,12 @@ llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group
  * shards resident on this device copied back to host_dst[g] (entries of ranks
  * on other devices are ignored; host buffers should be pinned).  Pipelined per
  * layer group on two library-owned copy streams: H2D of group g+1 and D2H of
- * group g-1 overlap the kernels of group g.  When `stream` passes the end of
- * the call, every host_dst byte of this device's generator ranks is written. */
+ * group g-1 overlap the kernels of group g (decoder layers open and close the
+ * pipeline; the embedding and lm_head groups run in its middle).  NVFP4 plans
+ * are not pipelined (whole buffers in, the whole sync, whole buffers out on
+ * `stream`: a tensor's scale needs its whole amax).  When `stream` passes the
+ * end of the call, every host_dst byte of this device's generator ranks is
+ * written. */
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device,
                            const void *const *host_src, void *const *host_dst,
                            void *const *src_ptrs, void *const *dst_ptrs, void *stream);

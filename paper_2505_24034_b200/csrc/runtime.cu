@@ -240,6 +240,20 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
 
 // Enqueue cast items [c0, c1) and fp8 items [f0, f1); the last launch signals
 // every device in `sig` (its last CTA, after all CTAs' stores are fenced).
+// Every device table ensure_uploaded allocates (plan destroy, re-upload).
+static void free_device_tables(DeviceWork &W) {
+    void **ptrs[] = {reinterpret_cast<void **>(&W.d_items), reinterpret_cast<void **>(&W.d_segs),
+                     reinterpret_cast<void **>(&W.d_done), reinterpret_cast<void **>(&W.d_tma_refs),
+                     reinterpret_cast<void **>(&W.d_tmaps), reinterpret_cast<void **>(&W.d_nv_partial),
+                     reinterpret_cast<void **>(&W.d_nv_amax), reinterpret_cast<void **>(&W.d_nv_contrib),
+                     reinterpret_cast<void **>(&W.d_nv_tensor_dev), reinterpret_cast<void **>(&W.d_nv_local),
+                     reinterpret_cast<void **>(&W.d_nv_done)};
+    for (void **q : ptrs) {
+        cudaFree(*q);
+        *q = nullptr;
+    }
+}
+
 static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, KParams &kp, int64_t c0, int64_t c1,
                                  int64_t f0, int64_t f1, const std::vector<int> &sig, cudaStream_t s) {
     const bool has_fp8 = f1 > f0;
@@ -345,14 +359,21 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
     return LLRL_OK;
 }
 
+static llrl_status sync_body(llrl_plan *p, llrl_comm *comm, int device, KParams &kp, cudaStream_t s);
+
 llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs, void *const *dst_ptrs,
                       void *stream) {
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
     llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
     if (st != LLRL_OK) return st;
+    return sync_body(p, comm, device, kp, static_cast<cudaStream_t>(stream));
+}
+
+// The whole-sync launch sequence (llrl_sync; llrl_sync_host for NVFP4).
+static llrl_status sync_body(llrl_plan *p, llrl_comm *comm, int device, KParams &kp, cudaStream_t s) {
+    llrl_status st = LLRL_OK;
     DeviceWork &W = p->dev[size_t(device)];
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (p->nv) {
         st = nv_handshake(p, W, comm, device, kp, s);
         if (st != LLRL_OK) return st;
@@ -372,10 +393,9 @@ llrl_status llrl_plan_set_max_ctas(llrl_plan *p, int device, int max_ctas) {
     if (!p || device < 0 || device >= p->n_devices || max_ctas < 0) { set_error("invalid argument"); return LLRL_E_INVALID; }
     DeviceWork &W = p->dev[size_t(device)];
     W.max_ctas = max_ctas;
-    if (W.uploaded_device >= 0) {
-        DeviceGuard guard(device);
-        cudaFree(W.d_items); cudaFree(W.d_segs); cudaFree(W.d_done); cudaFree(W.d_tma_refs); cudaFree(W.d_tmaps);
-        W.d_items = nullptr; W.d_segs = nullptr; W.d_done = nullptr; W.d_tma_refs = nullptr; W.d_tmaps = nullptr;
+    if (W.uploaded_device >= 0) {           // re-upload (grid sizes) at the next sync
+        DeviceGuard guard(W.uploaded_device);
+        free_device_tables(W);
         W.tmap_src.clear();
         W.uploaded_device = -1;
     }
@@ -440,7 +460,6 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void *const *host_src,
                            void *const *host_dst, void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
     if (!host_src || !host_dst) { set_error("llrl_sync_host: invalid argument"); return LLRL_E_INVALID; }
-    if (p && p->nv) { set_error("llrl_sync_host: NVFP4 needs whole-tensor amax -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
     llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
@@ -467,6 +486,21 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
     CK(cudaEventRecord(ev(size_t(2 * G)), s));
     CK(cudaStreamWaitEvent(h2d, ev(size_t(2 * G)), 0));
     CK(cudaStreamWaitEvent(d2h, ev(size_t(2 * G)), 0));
+    if (p->nv) {
+        // NVFP4 (R16): a tensor's scale needs its whole amax, so no per-group
+        // pipelining: every trainer byte in, the whole sync, every generator byte out
+        for (int r = 0; r < p->n_src; r++)
+            if (p->src_device[size_t(r)] == device && host_src[r])
+                CK(cudaMemcpyAsync(src_ptrs[r], host_src[r], size_t(p->src_rank_bytes[size_t(r)]),
+                                   cudaMemcpyHostToDevice, s));
+        st = sync_body(p, comm, device, kp, s);
+        if (st != LLRL_OK) return st;
+        for (int q = 0; q < p->n_dst; q++)
+            if (p->dst_device[size_t(q)] == device && host_dst[q])
+                CK(cudaMemcpyAsync(host_dst[q], dst_ptrs[q], size_t(p->dst_rank_bytes[size_t(q)]),
+                                   cudaMemcpyDeviceToHost, s));
+        return LLRL_OK;
+    }
     // Group order: the first group's H2D and the last group's D2H are not
     // overlapped with anything, so the (large) embedding and lm_head groups go
     // to the middle of the pipeline and decoder layers open and close it.  Every
@@ -531,17 +565,7 @@ void llrl_plan_destroy(llrl_plan *p) {
         DeviceWork &W = p->dev[d];
         if (W.uploaded_device < 0) continue;
         DeviceGuard guard(W.uploaded_device);
-        cudaFree(W.d_items);
-        cudaFree(W.d_segs);
-        cudaFree(W.d_done);
-        cudaFree(W.d_tma_refs);
-        cudaFree(W.d_tmaps);
-        cudaFree(W.d_nv_partial);
-        cudaFree(W.d_nv_amax);
-        cudaFree(W.d_nv_contrib);
-        cudaFree(W.d_nv_tensor_dev);
-        cudaFree(W.d_nv_local);
-        cudaFree(W.d_nv_done);
+        free_device_tables(W);
         for (void *e : W.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         if (W.h2d_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.h2d_stream));
         if (W.d2h_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.d2h_stream));

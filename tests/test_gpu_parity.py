@@ -533,7 +533,8 @@ def test_toy_parity_cuda_graph_replay_nvfp4(rt, sdt, f, tt, tg):
 
 
 @pytest.mark.parametrize("sdt,ddt,f,tt,tg", [("f32", "bf16", 2, 1, 2), ("bf16", "fp8", 2, 2, 8),
-                                           ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8)])
+                                           ("bf16", "mxfp8", 2, 2, 8), ("bf16", "mxfp4", 2, 2, 8),
+                                           ("bf16", "nvfp4", 2, 2, 8), ("f32", "nvfp4", 3, 1, 4)])
 def test_toy_parity_sync_host(rt, sdt, ddt, f, tt, tg):
     """llrl_sync_host: pinned host trainer shards in, host generator shards out,
     pipelined per layer group; twice, to exercise stream/event reuse."""
