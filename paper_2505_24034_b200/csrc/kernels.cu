@@ -580,13 +580,13 @@ __global__ void __launch_bounds__(kThreads + 32, MINB) llrl_k_fp8_tma(const __gr
     complete(P);
 }
 
-// ---- K1b: TMA-staged relayout + cast ---------------------------------------------
-// Warp-specialised like K2: warp 0 (producer) stages each item's rows into a
-// kCastStages-deep ring of 32 KiB shared-memory stages with cp.async.bulk
-// (mbarrier tx-count completion); warps 1..4 (workers) convert fp32 -> bf16
-// in shared memory when a cast is needed, and one worker thread writes each
-// stage back with cp.async.bulk shared -> global (local HBM or a peer GPU's
-// HBM over NVLink), releasing a stage once its bulk store has read it.  Data
+// ---- K1: TMA-staged relayout + cast / quantisation ------------------------------
+// Warp-specialised: warp 0 (producer) stages each item's rows into an NST-deep
+// ring of SB-byte shared-memory stages with cp.async.bulk (mbarrier tx-count
+// completion); warp 1 (storer) writes each converted stage back with
+// cp.async.bulk shared -> global (local HBM or a peer GPU's HBM over NVLink)
+// and releases it once the bulk store has read it; warps 2.. (NWK workers)
+// convert in shared memory (fp32 -> bf16, MXFP8 / MXFP4 / NVFP4 groups).  Data
 // never passes through registers on identity copies (bf16 -> bf16).
 
 // TMA cast kernel configurations: (stage bytes, stages, worker threads, CTAs/SM)
