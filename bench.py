@@ -250,17 +250,27 @@ def run_llrl(args):
     for _ in range(args.warmup):
         job.sync()
     _barrier()
+    # working sets that could stay in the 126 MB L2 between syncs are measured one
+    # sync at a time with L2 flushed before each (timing rule); larger ones stream
+    ws = max(job.plan.device_bytes(d)["hbm_read"] + job.plan.device_bytes(d)["hbm_write"]
+             for d in range(job.plan.stats().n_devices))
+    small = ws < (1 << 30)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=torch.device("cuda", local)) if small else None
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler([local]) as clk:
         time.sleep(0.25)       # let the sampler start before the timed region
         _barrier()
-        if args.step_sync:
+        if args.step_sync or small:
             # isolated syncs: every GPU idle and every rank past a barrier before each
-            # one, so no sync overlaps the previous one's tail (single-sync latency)
+            # one, so no sync overlaps the previous one's tail (single-sync latency);
+            # small working sets: L2 flushed (a 512 MB write) before each sync
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(args.steps)]
             for k in range(args.steps):
+                if small:
+                    with torch.cuda.stream(stream):
+                        flush.fill_(k & 0xFF)
                 torch.cuda.synchronize()
                 _barrier()
                 with torch.cuda.stream(stream):
@@ -276,7 +286,7 @@ def run_llrl(args):
                     job.sync()
                     ev[k + 1].record(stream)
         _barrier()
-    if args.step_sync:
+    if args.step_sync or small:
         step_ms = [_allmax(a.elapsed_time(b)) for a, b in evs]
         ms = sum(step_ms) / len(step_ms)
         ms_min = min(step_ms)
@@ -344,13 +354,14 @@ def run_llrl(args):
                        "max_ctas": args.max_ctas or "all SMs",
                        "multicast": bool(args.multicast and job.mc_positions()[0]),
                        "replicate": args.replicate,
-                       "timing": "isolated syncs (barrier before each)" if args.step_sync else "back-to-back syncs",
+                       "timing": "isolated syncs (barrier before each)" if (args.step_sync or small) else "back-to-back syncs",
                        "regime": ("all ranks on one GPU: local HBM re-layout + cast" if args.gpus == 1 else
                                   f"{cfg.placement} placement over {args.gpus} GPUs: fused pushes over NVLink"
                                   " (G=1 and G>=2 are different regimes; compare each to roofline.t_lb_ms)"),
                        "n_layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
                        "tp_gen": cfg.tp_gen, "placement": cfg.placement,
-                       "l2": "inputs >> 126 MB L2 (no flush needed)"},
+                       "l2": ("working set < 1 GB: L2 flushed (512 MB write) before every timed sync, syncs "
+                              "timed one at a time" if small else "inputs >> 126 MB L2 (no flush needed)")},
             "throughput": {"gen_bytes_per_s_GB": round(tot.dst_bytes / (ms * 1e6), 1),
                            "algorithmic_bytes_GB": round((tot.src_bytes + tot.dst_bytes) / 1e9, 3),
                            "nvlink_wire_GB": round(wire / 1e9, 3),
