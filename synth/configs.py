@@ -89,6 +89,10 @@ CONFIGS = {
                         notes="70B bf16 TP=8 -> MXFP4 TP=8 (E2M1 + E8M0 per 1x32)"),
     "c11": LayoutConfig("c11", "llama3-70b", 1, 8, 8, "bf16", "nvfp4", "colocated",
                         notes="70B bf16 TP=8 -> NVFP4 TP=8 (E2M1 + E4M3 per 1x16 + fp32 per tensor)"),
+    # NVFP4 with the per-tensor amax reduced across GPUs: FSDP=8 chunks of every
+    # generator tensor sit on several GPUs (the cross-GPU handshake of R16)
+    "c12": LayoutConfig("c12", "llama3-70b", 8, 1, 8, "bf16", "nvfp4", "colocated",
+                        notes="70B bf16 FSDP=8 -> NVFP4 TP=8 (cross-GPU tensor amax)"),
     # NEXT f1 with NVLS multicast: more generator replicas than trainer GPUs, so the
     # trainer's NVLink egress binds without multicast (3 copies) and not with it (1 copy).
     "c9": LayoutConfig("c9", "llama3-8b", 1, 1, 1, "bf16", "bf16", "fanout", dp_gen=3,

@@ -309,7 +309,7 @@ def main():
     if rank0():
         print("ok nccl replicas", flush=True)
     if "--full" in sys.argv:
-        for name in ("c2", "c3", "c4", "c5", "c7", "c8", "c10", "c11"):
+        for name in ("c2", "c3", "c4", "c5", "c7", "c8", "c10", "c11", "c12"):
             full_case(runner, world, name)
             if dist.get_rank() == 0:
                 print("ok full", name, flush=True)
