@@ -395,6 +395,16 @@ def test_full_c11_70b_nvfp4_sampled(rt):
     job.close()
 
 
+def test_full_c12_70b_nvfp4_fsdp_sampled(rt):
+    """C12 (70B bf16 FSDP=8 -> NVFP4 TP=8: every generator tensor gathered from
+    eight FSDP chunks, strided o / down tiles) at G=1, 40-layer slice."""
+    job = _full_job(rt, "c12")
+    job.sync()
+    torch.cuda.synchronize()
+    _sampled_check(job, n_samples=2000, n_blocks=2)
+    job.close()
+
+
 def test_full_c3_70b_bf16_sampled(rt):
     """C3 (70B bf16 FSDP=8 -> bf16 TP=8) at G=1, 8-layer slice (memory)."""
     job = _full_job(rt, "c3", n_layers=8)
