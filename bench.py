@@ -133,96 +133,164 @@ def _barrier():
 
 
 # ---------------------------------------------------------------- CPU oracle legs
-
-def _oracle_sample(cfg_name, seed=0, stages=1):
-    """A bounded sample of the workload for the CPU oracle: one decoder layer per
-    pipeline stage of the config's model (no embed / lm_head), same layout parameters.  Returns
-    (oracle layout, src buffers, fraction of the full model's elements)."""
-    import numpy as np
-    import oracle
-    from synth import MODELS, CONFIGS
-    import math
-    cfg = CONFIGS[cfg_name]
-    full = MODELS[cfg.model]
-    per = math.lcm(cfg.pp_train, cfg.pp_gen)                                      # whole pipeline stages
-    m = full.replace(n_layers=min(full.n_layers, per * stages), with_embed=0)
-    ol = oracle.Layout(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
-                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
-    # cheap deterministic values keyed by (param, global row, col): replicated
-    # pieces agree, as the oracle requires (timing sample only)
-    src = []
-    for r in range(ol.n_src):
-        buf = np.zeros(ol.src_rank_bytes(r), np.uint8)
-        for p in range(ol.n_src_params):
-            off, r0, r1, c0, c1 = ol.src_piece(r, p)
-            if r1 <= r0 or c1 <= c0:
-                continue
-            rows = np.arange(r0, r1, dtype=np.int64)[:, None]
-            cols = np.arange(c0, c1, dtype=np.int64)[None, :]
-            v = (((rows * 131 + cols * 7 + p * 17 + seed) % 1021) - 510).astype(np.float32) * np.float32(2.0 ** -14)
-            if cfg.src_dtype == "bf16":
-                v = (v.view(np.uint32) >> 16).astype(np.uint16)
-            b = v.view(np.uint8).reshape(-1)
-            buf[off:off + b.size] = b
-        src.append(buf)
-    def count(mm):
-        L = oracle.Layout(mm, 1, 1, 1)
-        return sum(L.src_param_info(p)[0] * L.src_param_info(p)[1] for p in range(L.n_src_params))
-    frac = count(m) / count(full)
-    ol.n_layers_sample = m.n_layers
-    return ol, src, frac
+#
+# SURVEY §8(d) "How to time the oracle": the oracle (oracle/oracle.c, as it
+# stands) on host copies of the trainer shards of the WHOLE workload, timed
+# single-threaded and parameter-parallel (one generator parameter per task,
+# nproc threads: the "std::thread x nproc" leg; ctypes releases the GIL), with
+# nproc and the lscpu model stated.  The inputs are generated on the host by
+# synth.fast (the input generator) at the oracle's offsets -- nothing of the
+# product is loaded on these legs.
 
 
-def _time_oracle_once(ol, src):
-    import numpy as np
-    dst = [np.zeros(ol.dst_rank_bytes(g), np.uint8) for g in range(ol.n_dst)]
+def _model_for(cfg, n_gpus):
+    """The workload's model: runner.spec_for's rule (70B at G=1 is the 40-layer
+    slice with embed / lm_head), without importing the product."""
+    from synth import MODELS
+    m = MODELS[cfg.model]
+    return m.replace(n_layers=40) if cfg.model == "llama3-70b" and n_gpus == 1 else m
+
+
+def _cpu_model_name():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class OracleWorkload:
+    """Host trainer buffers of the whole workload + reusable generator buffers."""
+
+    def __init__(self, cfg, n_gpus, seed=0):
+        import numpy as np
+        import oracle
+        from synth import fast
+        self.model = _model_for(cfg, n_gpus)
+        ol = oracle.Layout(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype,
+                           cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+        assert ol.status == 0, ol.status
+        self.ol = ol
+        es = 4 if cfg.src_dtype == "f32" else 2
+        self.src = []
+        for r in range(ol.n_src):
+            buf = np.zeros(ol.src_rank_bytes(r), np.uint8)
+            for p in range(ol.n_src_params):
+                off, r0, r1, c0, c1 = ol.src_piece(r, p)
+                if r1 > r0 and c1 > c0:
+                    n = (r1 - r0) * (c1 - c0) * es
+                    fast.fill(buf[off:off + n], seed, p, ol.src_param_info(p)[2] == 2, cfg.src_dtype, r0, r1, c0, c1)
+            self.src.append(buf)
+        self.dst = [np.zeros(ol.dst_rank_bytes(q), np.uint8) for q in range(ol.n_dst)]
+        self.saddr = [b.ctypes.data for b in self.src]
+        self.daddr = [b.ctypes.data for b in self.dst]
+        # biggest generator params first so the thread pool's tail is short
+        size = [sum(ol.dst_param(q, gp)[0] * ol.dst_param(q, gp)[1] for q in range(min(ol.n_dst, 1)))
+                for gp in range(ol.n_dst_params)]
+        self.order = sorted(range(ol.n_dst_params), key=lambda gp: -size[gp])
+        self.elements = sum(ol.src_param_info(p)[0] * ol.src_param_info(p)[1] for p in range(ol.n_src_params))
+
+    def run(self, threads):
+        """One whole sync by the oracle; returns wall seconds."""
+        import concurrent.futures as cf
+        ol = self.ol
+        t0 = time.perf_counter()
+        if threads <= 1:
+            rc = ol.sync_addrs(self.saddr, self.daddr, (0, ol.n_dst_params))
+            assert rc == 0, rc
+        else:
+            with cf.ThreadPoolExecutor(threads) as ex:
+                rcs = list(ex.map(lambda gp: ol.sync_addrs(self.saddr, self.daddr, (gp, gp + 1)), self.order))
+            assert all(rc == 0 for rc in rcs), rcs
+        return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, n_gpus, single_thread=True):
+    """The oracle on the whole workload: parameter-parallel over nproc threads (the
+    reported value), and single-threaded (also the whole workload)."""
+    nproc = os.cpu_count() or 1
     t0 = time.perf_counter()
-    rc = ol.sync(src, dst)
-    dt = time.perf_counter() - t0
-    assert rc == 0, rc
-    return dt
-
-
-def cpu_baseline(cfg_name, full_model_name, target_s=12.0):
-    """The oracle on a bounded sample sized for ~10-30 s of host CPU work: one
-    decoder layer calibrates, then enough layers for ~target_s seconds run."""
-    ol, src, frac = _oracle_sample(cfg_name)
-    t1 = _time_oracle_once(ol, src)
-    k = max(1, min(64, int(round(target_s / max(t1, 1e-3)))))
-    if k > 1:
-        ol, src, frac = _oracle_sample(cfg_name, stages=k)
-    dt = _time_oracle_once(ol, src)
-    return {"value": round(dt / frac * 1e3, 3), "unit": "ms", "cores": 1, "kind": "oracle",
-            "sample": f"{ol.n_layers_sample} decoder layer(s) of {full_model_name} ({frac * 100:.2f}% of the elements), "
-                      f"oracle/oracle.c single-threaded on {os.cpu_count()} host cores; "
-                      f"{dt:.2f} s measured, extrapolated linearly to the whole model"}
+    w = OracleWorkload(cfg, n_gpus)
+    t_gen = time.perf_counter() - t0
+    par = w.run(nproc)
+    out = {"value": round(par * 1e3, 1), "unit": "ms", "cores": nproc, "kind": "oracle",
+           "sample": f"the whole workload ({w.model.n_layers} layers + embed/lm_head of {cfg.model}, "
+                     f"{w.elements / 1e9:.3f} G trainer elements), no extrapolation: oracle/oracle.c "
+                     f"parameter-parallel (one generator parameter per task) on {nproc} threads; host "
+                     f"{_cpu_model_name()}, nproc {nproc}; inputs generated on the host by synth.fast at the "
+                     f"oracle's offsets ({t_gen:.1f} s, not timed)",
+           "cpu_model": _cpu_model_name(), "nproc": nproc, "parallel_ms": round(par * 1e3, 1)}
+    if single_thread:
+        st = w.run(1)
+        out["single_thread_ms"] = round(st * 1e3, 1)
+        out["parallel_speedup"] = round(st / par, 2)
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle timed as it stands on the host (rank 0 only)."""
-    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """--impl reference: the CPU oracle as it stands on the host cores (rank 0
+    only): every step one whole sync of the workload, parameter-parallel over
+    nproc threads -- no sample, no extrapolation."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from synth import CONFIGS
     cfg = CONFIGS[args.config]
-    ol, src, frac = _oracle_sample(args.config)
+    nproc = os.cpu_count() or 1
+    w = OracleWorkload(cfg, args.gpus)
     for _ in range(args.warmup):
-        _time_oracle_once(ol, src)
-    ts = [_time_oracle_once(ol, src) for _ in range(args.steps)]
-    step_ms = sum(ts) / len(ts) / frac * 1e3
-    sample = (f"{ol.n_layers_sample} decoder layer(s) of {cfg.model} per step ({frac * 100:.2f}% of the elements), "
-              f"extrapolated linearly to the whole model; oracle/oracle.c single-threaded")
+        w.run(nproc)
+    ts = [w.run(nproc) for _ in range(args.steps)]
+    step_ms = sum(ts) / len(ts) * 1e3
+    sample = (f"every step the whole workload ({w.model.n_layers} layers + embed/lm_head of {cfg.model}, "
+              f"{w.elements / 1e9:.3f} G trainer elements): oracle/oracle.c parameter-parallel on {nproc} threads "
+              f"(host {_cpu_model_name()}); no extrapolation")
     line = {"impl": "reference", "metric": METRIC, "value": round(step_ms, 3), "unit": "ms",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}",
-            "data": "synthetic", "config": {"workload": _workload_name(cfg, args.gpus), "layout": cfg.notes},
-            "cpu_baseline": {"value": round(step_ms, 3), "unit": "ms", "cores": 1, "kind": "oracle", "sample": sample},
+            "ms_min": round(min(ts) * 1e3, 3), "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": DATA, "config": config_dict(cfg, args, w.model),
+            "cpu_baseline": {"value": round(step_ms, 3), "unit": "ms", "cores": nproc, "kind": "oracle",
+                             "sample": sample, "cpu_model": _cpu_model_name(), "nproc": nproc},
             "e2e": {"value": round(step_ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+DATA = "synthetic (counter-based Llama-init-scale weights)"
+
+
 def _workload_name(cfg, n):
     return f"{cfg.name}: {cfg.notes} @ {n} GPU(s)"
+
+
+def _small_working_set(cfg, model, n_gpus):
+    """Syncs whose per-GPU bytes could stay in the 126 MB L2 are timed one at a time
+    with L2 flushed before each (timing rule); decided from the layouts only, so
+    both arms report the same config."""
+    import oracle
+    ol = oracle.Layout(model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+    tot = sum(ol.src_rank_bytes(r) for r in range(ol.n_src)) + sum(ol.dst_rank_bytes(q) for q in range(ol.n_dst))
+    return tot / n_gpus < (1 << 30)
+
+
+def config_dict(cfg, args, model):
+    """The `config` object of both arms' JSON lines (identical for one invocation)."""
+    small = _small_working_set(cfg, model, args.gpus)
+    return {"workload": _workload_name(cfg, args.gpus), "shapes": cfg.model,
+            "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
+            "max_ctas": args.max_ctas or "all SMs", "multicast": bool(args.multicast),
+            "replicate": args.replicate,
+            "timing": "isolated syncs (barrier before each)" if (args.step_sync or small) else "back-to-back syncs",
+            "regime": ("all ranks on one GPU: local HBM re-layout + cast" if args.gpus == 1 else
+                       f"{cfg.placement} placement over {args.gpus} GPUs: fused pushes over NVLink"
+                       " (G=1 and G>=2 are different regimes; compare each to roofline.t_lb_ms)"),
+            "n_layers": model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
+            "tp_gen": cfg.tp_gen, "placement": args.placement or cfg.placement,
+            "l2": ("working set < 1 GB: L2 flushed (512 MB write) before every timed sync, syncs "
+                   "timed one at a time" if small else "inputs >> 126 MB L2 (no flush needed)")}
 
 
 # ---------------------------------------------------------------- our arm
@@ -252,9 +320,7 @@ def run_llrl(args):
     _barrier()
     # working sets that could stay in the 126 MB L2 between syncs are measured one
     # sync at a time with L2 flushed before each (timing rule); larger ones stream
-    ws = max(job.plan.device_bytes(d)["hbm_read"] + job.plan.device_bytes(d)["hbm_write"]
-             for d in range(job.plan.stats().n_devices))
-    small = ws < (1 << 30)
+    small = _small_working_set(cfg, job.model, args.gpus)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=torch.device("cuda", local)) if small else None
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -329,6 +395,13 @@ def run_llrl(args):
     roof["binding_gpu"] = bdev
     if args.replicate == "nccl":
         roof["note"] = "bytes of the fused replica-0 sync only; the NCCL broadcasts come on top"
+    if info.nv_amax_read_bytes:
+        roof["nv_amax_pass_reread_bytes"] = info.nv_amax_read_bytes
+        roof["note"] = ("NVFP4 two-pass sync: achieved counts the algorithmic bytes (each source read once + "
+                        "every generator byte written); the per-tensor amax pass re-reads "
+                        f"{info.nv_amax_read_bytes / 1e9:.2f} GB on top (in `traffic`, not in `achieved`); "
+                        "see nvfp4_supplied_amax for the one-pass sync")
+    nv1 = _nv_supplied(job, args, nbytes, peak) if cfg.dst_dtype == "nvfp4" and not args.no_nv_supplied else None
 
     # end to end through the C ABI with host buffers (pinned), copies in the timed region
     e2e = None
@@ -348,20 +421,8 @@ def run_llrl(args):
             "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "ms_min": round(ms_min, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": "synthetic (counter-based Llama-init-scale weights)",
-            "config": {"workload": _workload_name(cfg, args.gpus), "shapes": cfg.model,
-                       "dp_gen": cfg.dp_gen, "pp_train": cfg.pp_train, "pp_gen": cfg.pp_gen,
-                       "max_ctas": args.max_ctas or "all SMs",
-                       "multicast": bool(args.multicast and job.mc_positions()[0]),
-                       "replicate": args.replicate,
-                       "timing": "isolated syncs (barrier before each)" if (args.step_sync or small) else "back-to-back syncs",
-                       "regime": ("all ranks on one GPU: local HBM re-layout + cast" if args.gpus == 1 else
-                                  f"{cfg.placement} placement over {args.gpus} GPUs: fused pushes over NVLink"
-                                  " (G=1 and G>=2 are different regimes; compare each to roofline.t_lb_ms)"),
-                       "n_layers": job.model.n_layers, "fsdp": cfg.fsdp, "tp_train": cfg.tp_train,
-                       "tp_gen": cfg.tp_gen, "placement": cfg.placement,
-                       "l2": ("working set < 1 GB: L2 flushed (512 MB write) before every timed sync, syncs "
-                              "timed one at a time" if small else "inputs >> 126 MB L2 (no flush needed)")},
+            "dtype": f"{cfg.src_dtype}->{cfg.dst_dtype}", "data": DATA,
+            "config": config_dict(cfg, args, job.model),
             "throughput": {"gen_bytes_per_s_GB": round(tot.dst_bytes / (ms * 1e6), 1),
                            "algorithmic_bytes_GB": round((tot.src_bytes + tot.dst_bytes) / 1e9, 3),
                            "nvlink_wire_GB": round(wire / 1e9, 3),
@@ -376,8 +437,11 @@ def run_llrl(args):
             line["comparator"] = comp
         if ovl:
             line["overlap"] = ovl
+        if nv1:
+            line["nvfp4_supplied_amax"] = nv1
         if not args.no_cpu_baseline and args.gpus == 1:      # rank 0 at N=1 only
-            line["cpu_baseline"] = cpu_baseline(args.config, cfg.model)
+            job.close()                                     # free the GPU job first (host RAM: pinned e2e)
+            line["cpu_baseline"] = cpu_baseline(cfg, args.gpus, single_thread=not args.no_cpu_single)
         print(json.dumps(line), flush=True)
     job.close()
     import torch.distributed as dist
@@ -419,6 +483,50 @@ def _e2e(job, args):
     d2h = int(_allsum(sum(t.numel() for t in host_dst.values())))
     return {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": steps, "api": "llrl_sync_host (C ABI, pinned host buffers)"}
+
+
+def _caller_nv_amax(job):
+    """The caller's side of llrl_sync_nv_amax (e.g. its optimizer epilogue): max |x|
+    of every NVFP4 tensor over the trainer regions the plan lists, with torch,
+    MAX-reduced over processes.  Not part of the timed sync."""
+    import torch
+    import torch.distributed as dist
+    n = job.plan.nv_num_tensors()
+    amax = torch.zeros(max(1, n), dtype=torch.float32, device=torch.device("cuda", job.device))
+    dt = torch.float32 if job.cfg.src_dtype == "f32" else torch.bfloat16
+    for tid in range(n):
+        for s in job.plan.nv_tensor_sources(tid):
+            t = job.src.get(s.src_rank)
+            if t is not None:
+                v = t.view(dt).as_strided((s.rows, s.cols), (s.src_ld, 1), s.src_off)
+                amax[tid] = torch.maximum(amax[tid], v.abs().max().float())
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+    return amax
+
+
+def _nv_supplied(job, args, nbytes, peak):
+    """NVFP4 through llrl_sync_nv_amax (one pass: the per-tensor amax supplied by
+    the caller), timed like the main line (back-to-back, CUDA events, max over
+    ranks), against the same algorithmic bytes and peak."""
+    import torch
+    amax = _caller_nv_amax(job)
+    for _ in range(3):
+        job.sync_nv_amax(amax)
+    _barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, args.steps)
+    e0.record(job.stream)
+    for _ in range(steps):
+        job.sync_nv_amax(amax)
+    e1.record(job.stream)
+    _barrier()
+    ms = _allmax(e0.elapsed_time(e1) / steps)
+    ach = nbytes / ms / 1e6
+    return {"value": round(ms, 4), "unit": "ms", "steps": steps, "achieved": round(ach, 1), "peak": peak,
+            "frac": round(ach / peak, 4), "api": "llrl_sync_nv_amax (C ABI)",
+            "amax": "supplied by the caller (here torch max|x| over llrl_plan_nv_tensor_sources, outside the "
+                    "timed region -- in an RL step the optimizer epilogue produces it)"}
 
 
 def _overlap(job, args):
@@ -595,6 +703,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-single", action="store_true", help="cpu_baseline: skip the single-threaded pass")
+    ap.add_argument("--no-nv-supplied", action="store_true", help="NVFP4: skip the supplied-amax one-pass timing")
     ap.add_argument("--layers", type=int, default=None, help="override decoder layers (profiling only)")
     ap.add_argument("--placement", default=None, choices=["disjoint", "colocated", "rotated", "fanout"])
     ap.add_argument("--multicast", action="store_true", help="NVLS multicast to generator DP replicas (f1)")

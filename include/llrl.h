@@ -184,6 +184,10 @@ typedef struct {
     int32_t n_senders_in;  /* other devices writing into this device (it waits for them) */
     int32_t n_launches;    /* kernels llrl_sync enqueues on this device */
     int32_t reserved;
+    int64_t nv_amax_read_bytes;   /* NVFP4 two-pass sync: source bytes the per-tensor amax
+                                     pass re-reads on this device (on top of the algorithmic
+                                     hbm_read of llrl_plan_device_bytes; 0 with
+                                     llrl_sync_nv_amax) */
 } llrl_device_info;
 llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_info *out);
 
@@ -201,7 +205,12 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
  *   single process: llrl_comm_flag_ptr + llrl_comm_set_peer (peer access is
  *                  enabled by the library).
  * One comm per device per process; it may serve any number of plans, provided
- * every process issues the same sequence of llrl_sync calls. */
+ * every process issues the same sequence of llrl_sync calls.  Each NVFP4 plan
+ * takes its own region of the comm's amax table on its first llrl_sync on that
+ * device (regions are assigned in first-sync order, which the same-sequence
+ * rule makes identical on every process; they are not reused after
+ * llrl_plan_destroy); the table holds about 60k NVFP4 tensors per comm
+ * lifetime (UNSUPPORTED beyond). */
 llrl_status llrl_comm_create(int device, llrl_comm **out);
 llrl_status llrl_comm_export(const llrl_comm *c, void *handle64);
 llrl_status llrl_comm_import(llrl_comm *c, int peer_device, const void *handle64);
@@ -225,6 +234,78 @@ llrl_status llrl_mc_import(int fd, int n_devices, int64_t size, llrl_mcbuf **out
 llrl_status llrl_mc_join(llrl_mcbuf *m, int device, void **local_ptr, void **mc_ptr);
 void llrl_mc_destroy(llrl_mcbuf *m);
 llrl_status llrl_plan_set_multicast(llrl_plan *p, int device, void *const *dst_mc_ptrs);
+
+/* ---- NVFP4 with a caller-supplied tensor amax (R16 in one pass) ----------------
+ * llrl_sync on an NVFP4 plan reads every quantised source twice: a per-tensor
+ * amax pass (a max-reduction across every GPU feeding the tensor, done inside
+ * the sync) and the quantising pass.  A caller that already knows each
+ * generator tensor's amax -- e.g. its optimizer epilogue took max |w| while
+ * writing the updated shards ("stream layer l as soon as the optimizer updates
+ * it", NEXT f3) -- passes it to llrl_sync_nv_amax, which reads each
+ * source byte once (no amax pass, no handshake).
+ * The plan's NVFP4 generator tensors are numbered 0..n-1.  Tensor `tid` is
+ * generator param `dst_param` (canonical generator index) on generator rank
+ * `dst_rank`, held by GPU `device`; its elements are exactly the trainer
+ * regions llrl_plan_nv_tensor_sources lists (src_rank's buffer, element offset
+ * src_off, rows x cols with leading dimension src_ld; replicated pieces are
+ * listed once).  Errors: INVALID (not an NVFP4 plan, tid / range out of bounds). */
+typedef struct {
+    int32_t dst_rank, dst_param, device, n_sources;
+} llrl_nv_tensor;
+typedef struct {
+    int32_t src_rank, src_param;
+    int64_t src_off, rows, cols, src_ld;   /* elements of the trainer dtype */
+} llrl_nv_source;
+llrl_status llrl_plan_nv_num_tensors(const llrl_plan *p, int *n);
+llrl_status llrl_plan_nv_tensor(const llrl_plan *p, int tid, llrl_nv_tensor *out);
+llrl_status llrl_plan_nv_tensor_sources(const llrl_plan *p, int tid, int first, int count, llrl_nv_source *out);
+/* As llrl_sync, for an NVFP4 plan, with amax_dev[tid] (device memory on
+ * `device`, fp32, one per plan tensor id) = max |x| over generator tensor tid:
+ * the same array on every device; it must be +0 or a positive finite value.
+ * When `stream` passes the call, the device's generator shards are complete
+ * (codes, group scales and each local tensor's fp32 scale A / 2688 with
+ * A = max(amax, 2^-64)); the result is byte-identical to llrl_sync's when the
+ * supplied amax is the exact one.  `comm` may be NULL iff the device exchanges
+ * no data with peers. */
+llrl_status llrl_sync_nv_amax(llrl_plan *p, llrl_comm *comm, int device, const float *amax_dev,
+                              void *const *src_ptrs, void *const *dst_ptrs, void *stream);
+
+/* ---- a5: NCCL where the mapping is a plain replication ---------------------------
+ * north_star: "a fallback that uses NCCL broadcast/all-gather only where the
+ * trainer->generator mapping is a plain shard replication"; the paper's
+ * replication semantics are BROADCAST, "sent identically to each inbound
+ * process".  A plan created with LLRL_PLAN_NCCL takes the NCCL path in
+ * the two cases that are pure replication (readings R17, R18 of DESIGN.md):
+ *   broadcast: generator DP replicas (R12) whose replicas of a rank position
+ *     sit on pairwise different GPUs: the fused kernels write replica 0 only,
+ *     then ncclBroadcast copies replica 0's whole rank buffer to the others;
+ *   all-gather: an FSDP-only trainer (tp_train = pp = 1, fsdp = F >= 2, every
+ *     parameter's rows divisible by F) synced without a cast (same dtype) into
+ *     F generator replicas of tp_gen = 1 placed on the trainer ranks' GPUs
+ *     (replica f with trainer rank f): every generator tensor part is the
+ *     concatenation of the F row chunks, i.e. one ncclAllGather per source
+ *     parameter into its offset in the generator buffer -- no kernel of ours.
+ * Otherwise (or without the flag) the fused kernels do everything.
+ * llrl_nccl_unique_id: one process makes the id (128 bytes) and shares it;
+ * llrl_nccl_attach: EVERY process of the job calls it once per plan, with its
+ * GPU, its rank in [0, nranks) and nranks (a collective: it creates the
+ * library-owned NCCL communicator and the sub-communicators the plan needs);
+ * the communicators are destroyed with the plan.  Then llrl_sync enqueues the
+ * NCCL operations after (broadcast) or instead of (all-gather) the kernels.
+ * llrl_plan_nccl_info: the operations one device takes part in.
+ * Errors: UNSUPPORTED (libnccl.so.2 not loadable), CUDA (NCCL error text),
+ * NOPEER (llrl_sync on an NCCL plan before llrl_nccl_attach). */
+#define LLRL_PLAN_NCCL 2u
+typedef struct {
+    int32_t n_broadcasts;   /* ncclBroadcast calls per sync on this device (member of) */
+    int32_t n_allgathers;   /* ncclAllGather calls per sync on this device */
+    int64_t bytes;          /* bytes this device receives through them per sync */
+    int32_t mode;           /* 0 = kernels only, 1 = kernels + broadcast, 2 = all-gather only */
+    int32_t reserved;
+} llrl_nccl_info;
+llrl_status llrl_nccl_unique_id(void *id128);
+llrl_status llrl_nccl_attach(llrl_plan *p, int device, const void *id128, int rank, int nranks);
+llrl_status llrl_plan_nccl_info(const llrl_plan *p, int device, llrl_nccl_info *out);
 
 /* Synchronous check of the timeout flag (1 if any wait on this device gave up). */
 llrl_status llrl_comm_timed_out(const llrl_comm *c, int *timed_out);

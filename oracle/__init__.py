@@ -77,6 +77,8 @@ def lib():
         L.orc_dst_param.argtypes = [M, C, ctypes.c_int, ctypes.c_int, i64p, i64p, ip, i64p, i64p]
         L.orc_dst_element_source.argtypes = [M, C, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                              ctypes.c_int64, ip, i64p, i64p]
+        L.orc_dst_param_sources.argtypes = [M, C, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p]
         L.orc_sync.argtypes = [M, C, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_sync_range.argtypes = [M, C, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.orc_check.argtypes = [M, C]
@@ -203,6 +205,26 @@ class Layout:
                                           ctypes.byref(p), ctypes.byref(r), ctypes.byref(c))
         assert rc == 0
         return p.value, r.value, c.value
+
+    def dst_param_sources(self, g, gp):
+        """-> (src_param [R,C] int32, row [R,C] int64, col [R,C] int64): the source
+        element of every element of generator param gp on rank g."""
+        R, C = self.dst_param(g, gp)[:2]
+        p = np.empty((R, C), np.int32)
+        r = np.empty((R, C), np.int64)
+        c = np.empty((R, C), np.int64)
+        rc = lib().orc_dst_param_sources(ctypes.byref(self.m), ctypes.byref(self.c), g, gp, _ptr(p), _ptr(r), _ptr(c))
+        assert rc == 0, rc
+        return p, r, c
+
+    def sync_addrs(self, src_addrs, dst_addrs, gp_range):
+        """orc_sync_range on raw host addresses: src_addrs[r] / dst_addrs[q] are the
+        (virtual) bases of the rank buffers; only the bytes of the params in
+        gp_range are read / written, so a caller may pass ``slice address -
+        slice offset`` to stream one parameter at a time."""
+        S = (ctypes.c_void_p * len(src_addrs))(*src_addrs)
+        D = (ctypes.c_void_p * len(dst_addrs))(*dst_addrs)
+        return lib().orc_sync_range(ctypes.byref(self.m), ctypes.byref(self.c), S, D, gp_range[0], gp_range[1])
 
     def sync(self, src_bufs, dst_bufs, gp_range=None):
         """Run the oracle on host numpy uint8 buffers (dst written in place)."""

@@ -728,6 +728,27 @@ int orc_dst_element_source(const orc_model *m, const orc_cfg *c, int g, int gp,
     return ORC_E_INVALID;
 }
 
+/* orc_dst_element_source for every element of generator param gp on rank g,
+ * row-major (R*C entries in each output array).  A plain loop, for the
+ * exhaustive pin in tests/test_oracle_pins.py. */
+int orc_dst_param_sources(const orc_model *m, const orc_cfg *c, int g, int gp,
+                          int32_t *src_param, int64_t *row, int64_t *col)
+{
+    int64_t R, C, off, soff; int qt;
+    int rc = orc_dst_param(m, c, g, gp, &R, &C, &qt, &off, &soff);
+    if (rc)
+        return rc;
+    for (int64_t lr = 0; lr < R; lr++)
+        for (int64_t lc = 0; lc < C; lc++) {
+            int p;
+            int64_t i = lr * C + lc;
+            if ((rc = orc_dst_element_source(m, c, g, gp, lr, lc, &p, &row[i], &col[i])))
+                return rc;
+            src_param[i] = p;
+        }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* The sync                                                                  */
 /* ------------------------------------------------------------------------ */

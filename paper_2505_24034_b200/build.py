@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libllrl.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["layout.cpp", "plan.cpp", "runtime.cu", "kernels.cu", "init.cu", "multicast.cu"]
+SOURCES = ["layout.cpp", "plan.cpp", "runtime.cu", "kernels.cu", "init.cu", "multicast.cu", "nccl.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
@@ -31,8 +31,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_one(src):
         obj = os.path.join(BUILD, src + ".o")
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        if src.endswith(".cpp"):
-            cmd[1:1] = ["-x", "cu"] if False else []
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

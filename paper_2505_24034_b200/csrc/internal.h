@@ -175,6 +175,8 @@ struct DeviceWork {
     struct NvLocal { int32_t tid, dst_rank; int64_t tscale_off; };
     NvLocal *d_nv_local = nullptr;
     unsigned long long *d_nv_done = nullptr;
+    int64_t nv_table_off = -1;         // this plan's region of the comm's amax table (byte offset)
+    llrl_comm *own_comm = nullptr;     // library-owned comm of a one-device NVFP4 plan called with comm = NULL
     std::vector<char> src_touched, dst_touched;   // ranks this device's items read / write
     bool touched_valid = false;
     bool has_mc = false;
@@ -192,6 +194,7 @@ struct DeviceWork {
     std::vector<std::vector<int>> pull_from;      // per group: devices this device reads from
     std::vector<std::vector<int>> pull_to;        // per group: devices that read from this device
     int64_t hbm_read = 0, hbm_write = 0, nvl_tx = 0, nvl_rx = 0;
+    int64_t nv_amax_read = 0;          // NVFP4 two-pass: bytes the amax pre-pass re-reads (not algorithmic)
     // device-side state (lazily created by the runtime)
     int uploaded_device = -1;
     Item *d_items = nullptr;
@@ -219,6 +222,30 @@ struct llrl_plan {
     bool nv = false;                     // NVFP4 destination (R16)
     struct NvTensor { int32_t dst_rank, dst_param, device; int64_t tscale_off; };
     std::vector<NvTensor> nv_tensors;    // tensor id -> generator tensor
+    std::vector<std::vector<llrl_nv_source>> nv_sources;   // tensor id -> trainer regions (its tiles)
+    // a5: NCCL for plain replication (LLRL_PLAN_NCCL; R17, R18)
+    int nccl_mode = 0;                   // 0 kernels only, 1 kernels + broadcast, 2 all-gather only
+    struct NcclBcast {                   // replica 0 of a rank position -> the other replicas
+        int set;                         // index in nccl_sets (its sub-communicator)
+        int root_dev;
+        std::vector<int> dst_rank;       // per member device (nccl_sets[set] order)
+        int64_t bytes;
+    };
+    struct NcclGather {                  // one source parameter: F row chunks -> every replica
+        int src_param;
+        int64_t count;                   // elements per trainer rank
+        std::vector<int64_t> src_off, dst_off;   // bytes, per FSDP rank f / replica f
+    };
+    std::vector<NcclBcast> nccl_bcast;
+    std::vector<NcclGather> nccl_gather;
+    std::vector<std::vector<int>> nccl_sets;     // distinct device sets (sorted): one sub-communicator each
+    int nccl_elem_bytes = 0;
+    struct NcclState {
+        void *parent = nullptr;
+        std::vector<void *> sub;         // per set: ncclComm_t, or null if not a member
+        int rank = -1;
+    };
+    std::map<int, NcclState> nccl;       // per device (this process)
     int src_dtype, dst_dtype;
     std::vector<int> src_device, dst_device;
     std::vector<int64_t> src_rank_bytes, dst_rank_bytes;
@@ -239,4 +266,11 @@ struct llrl_comm {
     unsigned long long *flags = nullptr;
     unsigned long long *peer_flags[llrl::kMaxDevices] = {};
     bool ipc_opened[llrl::kMaxDevices] = {};
+    int64_t nv_next = -1;                // next free byte of the NVFP4 amax table (per-plan regions)
 };
+
+namespace llrl {
+// nccl.cpp (a5): this device's NCCL operations of one sync on `stream`; free the plan's communicators.
+llrl_status nccl_enqueue(llrl_plan *p, int device, void *const *src_ptrs, void *const *dst_ptrs, void *stream);
+void nccl_destroy(llrl_plan *p);
+}  // namespace llrl

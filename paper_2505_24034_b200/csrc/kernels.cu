@@ -689,9 +689,14 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
                 __syncwarp();
                 unsigned char *dst = stages + st * kStride;
-                for (int r = lane; r < c.nr; r += 32)
-                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
-                             uint32_t(c.nc * es), &full_bar[st]);
+                if (c.nc == it.src_ld) {          // rows contiguous in the source: one bulk copy
+                    if (lane == 0)
+                        bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
+                } else {
+                    for (int r = lane; r < c.nr; r += 32)
+                        bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                                 uint32_t(c.nc * es), &full_bar[st]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -725,10 +730,12 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 if (lane == 0) {
                     const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
-                    for (int r = 0; r < c.nr; r++) {
+                    // rows contiguous in the destination (chunk spans whole rows): one bulk store
+                    const int nrow = c.nc == it.dst_ld ? 1 : c.nr, nel = c.nc == it.dst_ld ? c.nr * c.nc : c.nc;
+                    for (int r = 0; r < nrow; r++) {
                         const int64_t e = it.dst_off + int64_t(c.r0 + r) * it.dst_ld + c.c0;   // element offset
-                        if (fp4) bulk_s2g(dbase + e / 2, out + r * c.nc / 2, uint32_t(c.nc / 2));
-                        else bulk_s2g(dbase + e * des, out + r * c.nc * des, uint32_t(c.nc * des));
+                        if (fp4) bulk_s2g(dbase + e / 2, out + r * c.nc / 2, uint32_t(nel / 2));
+                        else bulk_s2g(dbase + e * des, out + r * c.nc * des, uint32_t(nel * des));
                     }
                     bulk_commit();
                     bulk_wait_read<1>();              // the previous group has read its stage
@@ -925,9 +932,14 @@ __global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_nv_amax(const __grid_
                 if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
                 __syncwarp();
                 unsigned char *dst = stages + st * kNvStageBytes;
-                for (int r = lane; r < c.nr; r += 32)
-                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
-                             uint32_t(c.nc * es), &full_bar[st]);
+                if (c.nc == it.src_ld) {          // rows contiguous in the source: one bulk copy
+                    if (lane == 0)
+                        bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
+                } else {
+                    for (int r = lane; r < c.nr; r += 32)
+                        bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                                 uint32_t(c.nc * es), &full_bar[st]);
+                }
             }
         }
     } else {
@@ -1011,6 +1023,17 @@ __global__ void __launch_bounds__(kThreads) llrl_k_nv_fetch(const __grid_constan
     for (int j = threadIdx.x; j < P.n_contrib; j += kThreads) {
         const int tid = P.contrib[j];
         P.amax_out[tid] = P.tables[P.tensor_dev[tid]][tid * kNvTableStride + kMaxDevices];
+    }
+}
+
+// llrl_sync_nv_amax: the fp32 tensor scale A / 2688 of every local tensor from
+// the caller-supplied amax (the same formula as llrl_k_nv_scale, R16).
+__global__ void __launch_bounds__(kThreads) llrl_k_nv_tscale(const __grid_constant__ NvTscaleParams P) {
+    const auto *loc = static_cast<const DeviceWork::NvLocal *>(P.locals);
+    for (int j = threadIdx.x + blockIdx.x * kThreads; j < P.n_local; j += kThreads * gridDim.x) {
+        const float A = fmaxf(__uint_as_float(P.amax[loc[j].tid]), 0x1p-64f);
+        *reinterpret_cast<float *>(static_cast<char *>(P.dst[loc[j].dst_rank]) + loc[j].tscale_off) =
+            __fdiv_rn(A, 2688.0f);
     }
 }
 
@@ -1146,6 +1169,12 @@ cudaError_t launch_nv_scale(const NvScaleParams &P, cudaStream_t stream) {
 
 cudaError_t launch_nv_fetch(const NvFetchParams &P, cudaStream_t stream) {
     llrl_k_nv_fetch<<<1, kThreads, 0, stream>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nv_tscale(const NvTscaleParams &P, cudaStream_t stream) {
+    const int grid = std::max(1, std::min(64, (P.n_local + kThreads - 1) / kThreads));
+    llrl_k_nv_tscale<<<grid, kThreads, 0, stream>>>(P);
     return cudaGetLastError();
 }
 

@@ -65,17 +65,26 @@ struct NvFetchParams {
 cudaError_t launch_nv_amax(const NvAmaxParams &P, bool src_f32, int grid, cudaStream_t stream);
 cudaError_t launch_nv_scale(const NvScaleParams &P, cudaStream_t stream);
 cudaError_t launch_nv_fetch(const NvFetchParams &P, cudaStream_t stream);
+// llrl_sync_nv_amax: the fp32 tensor scale of every local tensor from a supplied amax.
+struct NvTscaleParams {
+    const void *locals;                // DeviceWork::NvLocal[n_local]
+    int n_local;
+    const uint32_t *amax;              // [n_tensors] (fp32 bits)
+    void *dst[kMaxRanks];
+};
+cudaError_t launch_nv_tscale(const NvTscaleParams &P, cudaStream_t stream);
 // comm buffer (u64 words): slot ranges of kMaxDevices counters each --
 // [0,16) data arrivals per sender, [16,32) "layer group staged" per device,
 // [32,48) NVFP4 partial amax arrivals per sender, [48,64) NVFP4 "tensor scales
 // ready" per receiver; [64] timeout flag; [128,192) expected counts per slot
-// (device-side, local); from byte kNvTableOffset: the NVFP4 amax table
-// (17 u32 per tensor: one partial per sender device, then the global amax).
+// (device-side, local); from byte kNvTableOffset: the NVFP4 amax tables, one
+// region per plan (17 u32 per tensor: one partial per sender device, then the
+// global amax).
 constexpr int kSlotData = 0, kSlotStaged = 16, kSlotNvAmax = 32, kSlotNvReady = 48, kNumSlots = 64;
 constexpr int kFlagTimeout = 64;
 constexpr int kFlagExpected = 128;
 constexpr int64_t kNvTableOffset = 4096;
-constexpr int64_t kCommBytes = 1 << 20;
+constexpr int64_t kCommBytes = 4 << 20;
 constexpr int kNvTableStride = kMaxDevices + 1;   // u32 per tensor
 struct WaitTargets {
     unsigned long long count[kNumSlots];   // arrivals to wait for per flag slot; 0 = none

@@ -56,6 +56,95 @@ struct Builder {
     }
     std::vector<std::vector<std::vector<int>>> mc_extra;   // [exec dev][group] -> replica devices to signal
 
+    // a5 broadcast (R17): replica d >= 1 of a rank position whose replicas sit on
+    // pairwise different GPUs is a byte copy of replica 0 -- left to ncclBroadcast.
+    bool nccl_replica(int g) const {
+        if (P->nccl_mode != 1) return false;
+        const int pos = g % n_pos();
+        if (g / n_pos() == 0) return false;
+        for (int a = 0; a < D->dp_gen; a++)
+            for (int b = a + 1; b < D->dp_gen; b++)
+                if (P->dst_device[size_t(a * n_pos() + pos)] == P->dst_device[size_t(b * n_pos() + pos)]) return false;
+        return true;
+    }
+
+    // a5 all-gather (R18): the whole sync is a plain replication of FSDP chunks.
+    bool allgather_eligible() const {
+        const int F = S->fsdp;
+        if (F < 2 || S->tp_train != 1 || S->pp_train != 1 || D->tp_gen != 1 || D->pp_gen != 1 || D->dp_gen != F) return false;
+        if (S->dtype != D->dtype || (D->dtype != LLRL_BF16 && D->dtype != LLRL_F32)) return false;
+        for (int f = 0; f < F; f++) {
+            if (P->src_device[size_t(f)] != P->dst_device[size_t(f)]) return false;
+            for (int h = f + 1; h < F; h++)
+                if (P->src_device[size_t(f)] == P->src_device[size_t(h)]) return false;
+        }
+        for (const SrcParam &sp : S->src_params)
+            if (sp.rows % F) return false;
+        return true;
+    }
+
+    int nccl_set(std::vector<int> devs) {
+        std::sort(devs.begin(), devs.end());
+        for (size_t k = 0; k < P->nccl_sets.size(); k++)
+            if (P->nccl_sets[k] == devs) return int(k);
+        P->nccl_sets.push_back(devs);
+        return int(P->nccl_sets.size()) - 1;
+    }
+
+    void account_copy(int from, int to, int64_t bytes) {
+        P->dev[size_t(to)].hbm_write += bytes;
+        P->dev[size_t(from)].hbm_read += bytes;
+        if (from != to) {
+            P->dev[size_t(from)].nvl_tx += bytes;
+            P->dev[size_t(to)].nvl_rx += bytes;
+        }
+        P->traffic[size_t(from) * P->n_devices + to] += bytes;
+        P->stats.src_bytes += bytes;
+        P->stats.dst_bytes += bytes;
+    }
+
+    void make_nccl_ops() {
+        if (P->nccl_mode == 2) {
+            const int F = S->fsdp;
+            P->nccl_elem_bytes = int(es_src);
+            std::vector<int> devs(P->src_device.begin(), P->src_device.begin() + F);
+            nccl_set(devs);
+            for (size_t p = 0; p < S->src_params.size(); p++) {
+                const Piece &sp0 = S->pieces[0][p];
+                // where the part of source param p lands in the generator (tp_gen = 1: whole rows)
+                int64_t doff = -1;
+                for (const Piece &pc : D->pieces[0])
+                    for (const DstPart &part : pc.parts)
+                        if (part.src_param == int(p)) doff = pc.byte_off + part.lr0 * pc.cols * es_src;
+                llrl_plan::NcclGather og;
+                og.src_param = int(p);
+                og.count = sp0.rows * sp0.cols;
+                for (int f = 0; f < F; f++) {
+                    og.src_off.push_back(S->pieces[size_t(f)][p].byte_off);
+                    og.dst_off.push_back(doff);
+                }
+                for (int f = 0; f < F; f++)
+                    for (int h = 0; h < F; h++) account_copy(devs[size_t(h)], devs[size_t(f)], og.count * es_src);
+                P->nccl_gather.push_back(og);
+            }
+            return;
+        }
+        for (int pos = 0; pos < n_pos(); pos++) {
+            if (!nccl_replica(n_pos() + pos)) continue;
+            std::vector<int> devs;
+            for (int d = 0; d < D->dp_gen; d++) devs.push_back(P->dst_device[size_t(d * n_pos() + pos)]);
+            llrl_plan::NcclBcast b;
+            b.set = nccl_set(devs);
+            b.root_dev = P->dst_device[size_t(pos)];
+            b.bytes = D->rank_bytes[size_t(pos)];
+            for (int dev : P->nccl_sets[size_t(b.set)])
+                for (int d = 0; d < D->dp_gen; d++)
+                    if (P->dst_device[size_t(d * n_pos() + pos)] == dev) b.dst_rank.push_back(d * n_pos() + pos);
+            for (int d = 1; d < D->dp_gen; d++) account_copy(b.root_dev, P->dst_device[size_t(d * n_pos() + pos)], b.bytes);
+            P->nccl_bcast.push_back(b);
+        }
+    }
+
     int holder(const std::vector<int> &members, int g) const {
         for (int r : members)
             if (P->src_device[r] == P->dst_device[g]) return r;   // same GPU first (R5)
@@ -65,6 +154,7 @@ struct Builder {
     llrl_status make_tiles() {
         const int nsrc = S->n_ranks;
         for (int g = 0; g < D->n_ranks; g++) {
+            if (P->nccl_mode == 2 || nccl_replica(g)) continue;   // a5: filled by NCCL (R17, R18)
             for (const Piece &pc : D->pieces[g]) {
                 const int64_t es_d = dtype_bytes(pc.dtype);
                 for (const DstPart &part : pc.parts) {
@@ -204,6 +294,9 @@ struct Builder {
             } else {
                 tid = f->second;
             }
+            if (P->nv_sources.size() <= size_t(tid)) P->nv_sources.resize(size_t(tid) + 1);
+            P->nv_sources[size_t(tid)].push_back(
+                llrl_nv_source{int32_t(t.src_rank), int32_t(t.src_param), t.src_off, t.rows, t.cols, t.src_ld});
             DeviceWork &E = P->dev[size_t(P->src_device[size_t(t.src_rank)])];
             if (std::find(E.nv_contrib.begin(), E.nv_contrib.end(), tid) == E.nv_contrib.end())
                 E.nv_contrib.push_back(tid);
@@ -225,10 +318,9 @@ struct Builder {
         }
         const int64_t n = t.rows * t.cols;
         account(sd, sd, dd, n * es_src, (fp4 ? n / 2 : n) + n / grp, false);
-        if (nv) {                       // R16: the per-tensor amax pass reads the source once more
-            P->dev[size_t(sd)].hbm_read += n * es_src;
-            P->stats.src_bytes += n * es_src;
-        }
+        // R16: the two-pass sync's per-tensor amax pass reads the source once more.
+        // Not algorithmic bytes (a sync given the amax reads it once): tracked apart.
+        if (nv) P->dev[size_t(sd)].nv_amax_read += n * es_src;
         return LLRL_OK;
     }
 
@@ -546,6 +638,7 @@ struct Builder {
                 auto &rg = P->dst_group_range[size_t(g)][size_t(group_of(dpd.kind, dpd.layer))];
                 widen(rg, pc.byte_off, pc.byte_off + data_bytes(pc.dtype, pc.rows * pc.cols));
                 if (pc.quantised) widen(rg, pc.scale_off, pc.scale_off + scale_grid_bytes(pc.dtype, pc.rows, pc.cols));
+                if (pc.tscale_off >= 0) widen(rg, pc.tscale_off, pc.tscale_off + 4);   // NVFP4 tensor scale
             }
         return LLRL_OK;
     }
@@ -603,8 +696,18 @@ llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, con
     b.P = P;
     b.es_src = dtype_bytes(src->dtype);
     b.es_dst = dtype_bytes(dst->dtype == LLRL_F32 ? LLRL_F32 : LLRL_BF16);
+    if (flags & LLRL_PLAN_NCCL) {
+        if (P->multicast) {
+            delete P;
+            set_error("llrl_plan_create: LLRL_PLAN_NCCL and LLRL_PLAN_MULTICAST are exclusive");
+            return LLRL_E_INVALID;
+        }
+        P->nccl_mode = b.allgather_eligible() ? 2 : dst->dp_gen >= 2 ? 1 : 0;
+    }
     llrl_status st = b.make_tiles();
     if (st == LLRL_OK) st = b.make_items();
+    if (st == LLRL_OK) b.make_nccl_ops();
+    if (st == LLRL_OK && P->nccl_mode == 1 && P->nccl_bcast.empty()) P->nccl_mode = 0;
     if (st != LLRL_OK) { delete P; return st; }
     P->stats.n_devices = P->n_devices;
     P->stats.n_src_ranks = P->n_src;

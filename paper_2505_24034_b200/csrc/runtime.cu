@@ -166,12 +166,13 @@ llrl_status ensure_tmaps(llrl_plan *p, DeviceWork &W, void *const *src_ptrs, cud
     return LLRL_OK;
 }
 
-// Which ranks a device's items touch (for pointer validation).
 // Which ranks a device's items touch (pointer validation); computed once.
-void touched_ranks(DeviceWork &W, int n_src, int n_dst) {
+void touched_ranks(const llrl_plan *p, DeviceWork &W) {
     if (W.touched_valid) return;
-    W.src_touched.assign(size_t(n_src), 0);
-    W.dst_touched.assign(size_t(n_dst), 0);
+    W.src_touched.assign(size_t(p->n_src), 0);
+    W.dst_touched.assign(size_t(p->n_dst), 0);
+    for (int32_t tid : W.nv_local)   // NVFP4: the fp32 tensor scale is written on the holder's device
+        W.dst_touched[size_t(p->nv_tensors[size_t(tid)].dst_rank)] = 1;
     for (const Item &it : W.items) {
         if (it.kind == K_FP8_MULTI) {
             for (int s = 0; s < it.src_rank; s++) W.src_touched[size_t(W.segs[size_t(it.src_off) + s].src_rank)] = 1;
@@ -189,15 +190,30 @@ extern "C" {
 
 // Common prologue of llrl_sync / llrl_sync_group / llrl_sync_host: validate,
 // fill the pointer tables, upload on first use.
-static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *const *src_ptrs,
-                            void *const *dst_ptrs, KParams *kp) {
+// nv_table: the NVFP4 two-pass handshake needs the comm's amax table even on one
+// device; a one-device plan called with comm = NULL gets a library-owned comm.
+static llrl_status prologue(llrl_plan *p, llrl_comm *&comm, int device, void *const *src_ptrs,
+                            void *const *dst_ptrs, KParams *kp, bool nv_table) {
     if (!p || !src_ptrs || !dst_ptrs || device < 0 || device >= p->n_devices) {
         set_error("llrl_sync: invalid argument (device %d of %d)", device, p ? p->n_devices : 0);
         return LLRL_E_INVALID;
     }
     DeviceWork &W = p->dev[size_t(device)];
-    bool cross = !W.signal_devices.empty() || W.n_senders_in > 0 || p->nv;   // NVFP4: amax table in the comm
+    bool cross = !W.signal_devices.empty() || W.n_senders_in > 0;
     for (size_t g = 0; g < W.pull_from.size(); g++) cross = cross || !W.pull_from[g].empty() || !W.pull_to[g].empty();
+    if (nv_table) {
+        bool remote = false;
+        for (int d : W.nv_targets) remote = remote || d != device;
+        for (int d : W.nv_senders) remote = remote || d != device;
+        if (!comm && !cross && !remote) {
+            if (!W.own_comm) {
+                llrl_status st = llrl_comm_create(device, &W.own_comm);
+                if (st != LLRL_OK) return st;
+            }
+            comm = W.own_comm;
+        }
+        cross = cross || remote || !comm;
+    }
     if (cross) {
         if (!comm || comm->device != device) {
             set_error("llrl_sync: device %d exchanges data with peers and needs its comm", device);
@@ -209,7 +225,7 @@ static llrl_status prologue(llrl_plan *p, llrl_comm *comm, int device, void *con
                 return LLRL_E_NOPEER;
             }
     }
-    touched_ranks(W, p->n_src, p->n_dst);
+    touched_ranks(p, W);
     const std::vector<char> &su = W.src_touched, &du = W.dst_touched;
     std::memset(kp, 0, sizeof *kp);
     for (int r = 0; r < p->n_src; r++) {
@@ -294,15 +310,23 @@ static llrl_status wait_arrivals(llrl_comm *comm, const std::vector<int> &devs, 
 
 // NVFP4 (R16) per-tensor amax handshake (see kernels.cu): partials -> owners,
 // owners reduce and publish, contributors fetch; all device-side, stream-ordered.
-static uint32_t *nv_table(llrl_comm *comm, int dev) {
-    return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(comm->peer_flags[dev]) + kNvTableOffset);
+// Each plan has its own table region (assigned on its first sync on a comm, in
+// the same order on every process -- the same-sequence rule of llrl.h).
+static uint32_t *nv_table(llrl_comm *comm, int dev, const DeviceWork &W) {
+    return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(comm->peer_flags[dev]) + W.nv_table_off);
 }
 
 static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, int device, const KParams &kp,
                                 cudaStream_t s) {
-    if (p->nv_tensors.size() * kNvTableStride * 4 > size_t(kCommBytes - kNvTableOffset)) {
-        set_error("NVFP4: %zu generator tensors exceed the comm's amax table", p->nv_tensors.size());
-        return LLRL_E_UNSUPPORTED;
+    if (W.nv_table_off < 0) {
+        const int64_t need = (int64_t(p->nv_tensors.size()) * kNvTableStride * 4 + 255) / 256 * 256;
+        if (comm->nv_next < 0) comm->nv_next = kNvTableOffset;
+        if (comm->nv_next + need > kCommBytes) {
+            set_error("NVFP4: %zu generator tensors exceed the comm's free amax table space", p->nv_tensors.size());
+            return LLRL_E_UNSUPPORTED;
+        }
+        W.nv_table_off = comm->nv_next;
+        comm->nv_next += need;
     }
     for (int d : W.nv_targets)
         if (!comm->peer_flags[d]) { set_error("NVFP4: no comm mapping for device %d", d); return LLRL_E_NOPEER; }
@@ -319,7 +343,7 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
         a.n_contrib = int(W.nv_contrib.size());
         a.tensor_dev = W.d_nv_tensor_dev;
         for (int d = 0; d < p->n_devices; d++)
-            if (comm->peer_flags[d]) a.tables[d] = nv_table(comm, d);
+            if (comm->peer_flags[d]) a.tables[d] = nv_table(comm, d, W);
         a.my_dev = device;
         a.n_signal = int(W.nv_targets.size());
         for (int i = 0; i < a.n_signal; i++) a.signal[i] = comm->peer_flags[W.nv_targets[size_t(i)]] + kSlotNvAmax + device;
@@ -337,7 +361,7 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
         std::memset(&c, 0, sizeof c);
         c.locals = W.d_nv_local;
         c.n_local = int(W.nv_local.size());
-        c.table = nv_table(comm, device);
+        c.table = nv_table(comm, device, W);
         for (int g = 0; g < p->n_dst; g++) c.dst[g] = kp.dst[g];
         c.n_signal = int(W.nv_senders.size());
         for (int i = 0; i < c.n_signal; i++) c.signal[i] = comm->peer_flags[W.nv_senders[size_t(i)]] + kSlotNvReady + device;
@@ -352,7 +376,7 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
         f.n_contrib = int(W.nv_contrib.size());
         f.tensor_dev = W.d_nv_tensor_dev;
         for (int d = 0; d < p->n_devices; d++)
-            if (comm->peer_flags[d]) f.tables[d] = nv_table(comm, d);
+            if (comm->peer_flags[d]) f.tables[d] = nv_table(comm, d, W);
         f.amax_out = W.d_nv_amax;
         CK(launch_nv_fetch(f, s));
     }
@@ -365,9 +389,13 @@ llrl_status llrl_sync(llrl_plan *p, llrl_comm *comm, int device, void *const *sr
                       void *stream) {
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
-    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp, p && p->nv);
     if (st != LLRL_OK) return st;
-    return sync_body(p, comm, device, kp, static_cast<cudaStream_t>(stream));
+    st = sync_body(p, comm, device, kp, static_cast<cudaStream_t>(stream));
+    if (st != LLRL_OK) return st;
+    // a5: replicas by ncclBroadcast once replica 0 is complete here (stream order
+    // after the completion wait), or the whole sync as ncclAllGathers (R17, R18)
+    return nccl_enqueue(p, device, src_ptrs, dst_ptrs, stream);
 }
 
 // The whole-sync launch sequence (llrl_sync; llrl_sync_host for NVFP4).
@@ -377,6 +405,61 @@ static llrl_status sync_body(llrl_plan *p, llrl_comm *comm, int device, KParams 
     if (p->nv) {
         st = nv_handshake(p, W, comm, device, kp, s);
         if (st != LLRL_OK) return st;
+    }
+    st = launch_ranges(p, W, comm, kp, 0, W.n_cast, W.n_cast, int64_t(W.items.size()), W.signal_devices, s);
+    if (st != LLRL_OK) return st;
+    return wait_arrivals(comm, W.senders, s);
+}
+
+// ---- NVFP4 with a caller-supplied tensor amax (one pass) ----------------------
+
+llrl_status llrl_plan_nv_num_tensors(const llrl_plan *p, int *n) {
+    if (!p || !n) { set_error("NULL argument"); return LLRL_E_INVALID; }
+    *n = int(p->nv_tensors.size());
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_nv_tensor(const llrl_plan *p, int tid, llrl_nv_tensor *out) {
+    if (!p || !out || tid < 0 || size_t(tid) >= p->nv_tensors.size()) {
+        set_error("llrl_plan_nv_tensor: invalid argument");
+        return LLRL_E_INVALID;
+    }
+    const llrl_plan::NvTensor &t = p->nv_tensors[size_t(tid)];
+    out->dst_rank = t.dst_rank;
+    out->dst_param = t.dst_param;
+    out->device = t.device;
+    out->n_sources = int32_t(p->nv_sources[size_t(tid)].size());
+    return LLRL_OK;
+}
+
+llrl_status llrl_plan_nv_tensor_sources(const llrl_plan *p, int tid, int first, int count, llrl_nv_source *out) {
+    if (!p || tid < 0 || size_t(tid) >= p->nv_tensors.size() || first < 0 || count < 0 || (count && !out) ||
+        size_t(first) + size_t(count) > p->nv_sources[size_t(tid)].size()) {
+        set_error("llrl_plan_nv_tensor_sources: invalid argument");
+        return LLRL_E_INVALID;
+    }
+    std::copy(p->nv_sources[size_t(tid)].begin() + first, p->nv_sources[size_t(tid)].begin() + first + count, out);
+    return LLRL_OK;
+}
+
+llrl_status llrl_sync_nv_amax(llrl_plan *p, llrl_comm *comm, int device, const float *amax_dev,
+                              void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
+    if (!p || !p->nv || !amax_dev) { set_error("llrl_sync_nv_amax: needs an NVFP4 plan and an amax array"); return LLRL_E_INVALID; }
+    DeviceGuard guard(device >= 0 ? device : 0);
+    KParams kp;
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp, false);
+    if (st != LLRL_OK) return st;
+    DeviceWork &W = p->dev[size_t(device)];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    kp.nv_amax = reinterpret_cast<const uint32_t *>(amax_dev);
+    if (!W.nv_local.empty()) {
+        NvTscaleParams t;
+        std::memset(&t, 0, sizeof t);
+        t.locals = W.d_nv_local;
+        t.n_local = int(W.nv_local.size());
+        t.amax = kp.nv_amax;
+        for (int g = 0; g < p->n_dst; g++) t.dst[g] = kp.dst[g];
+        CK(launch_nv_tscale(t, s));
     }
     st = launch_ranges(p, W, comm, kp, 0, W.n_cast, W.n_cast, int64_t(W.items.size()), W.signal_devices, s);
     if (st != LLRL_OK) return st;
@@ -418,9 +501,10 @@ llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group
                             void *const *dst_ptrs, void *stream) {
     if (!p || group < 0 || group >= p->n_groups) { set_error("llrl_sync_group: invalid group"); return LLRL_E_INVALID; }
     if (p->nv) { set_error("llrl_sync_group: NVFP4 needs whole-tensor amax -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
+    if (p->nccl_mode) { set_error("llrl_sync_group: NCCL replication is per rank buffer -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
-    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp, false);
     if (st != LLRL_OK) return st;
     DeviceWork &W = p->dev[size_t(device)];
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -450,6 +534,7 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
     for (const Item &it : W.items) out->n_fp8_pull_items += it.kind == K_FP8_MULTI;
     out->n_signal = int32_t(W.signal_devices.size());
     out->n_senders_in = W.n_senders_in;
+    out->nv_amax_read_bytes = W.nv_amax_read;
     return llrl_sync_num_launches(p, device, &out->n_launches);
 }
 
@@ -460,9 +545,10 @@ llrl_status llrl_plan_device_info(const llrl_plan *p, int device, llrl_device_in
 llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void *const *host_src,
                            void *const *host_dst, void *const *src_ptrs, void *const *dst_ptrs, void *stream) {
     if (!host_src || !host_dst) { set_error("llrl_sync_host: invalid argument"); return LLRL_E_INVALID; }
+    if (p && p->nccl_mode) { set_error("llrl_sync_host: not for LLRL_PLAN_NCCL plans -- use llrl_sync"); return LLRL_E_UNSUPPORTED; }
     DeviceGuard guard(device >= 0 ? device : 0);
     KParams kp;
-    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp);
+    llrl_status st = prologue(p, comm, device, src_ptrs, dst_ptrs, &kp, p && p->nv);
     if (st != LLRL_OK) return st;
     DeviceWork &W = p->dev[size_t(device)];
     const int G = p->n_groups;
@@ -561,6 +647,7 @@ llrl_status llrl_sync_host(llrl_plan *p, llrl_comm *comm, int device, const void
 
 void llrl_plan_destroy(llrl_plan *p) {
     if (!p) return;
+    nccl_destroy(p);
     for (size_t d = 0; d < p->dev.size(); d++) {
         DeviceWork &W = p->dev[d];
         if (W.uploaded_device < 0) continue;
@@ -569,6 +656,7 @@ void llrl_plan_destroy(llrl_plan *p) {
         for (void *e : W.events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         if (W.h2d_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.h2d_stream));
         if (W.d2h_stream) cudaStreamDestroy(static_cast<cudaStream_t>(W.d2h_stream));
+        if (W.own_comm) llrl_comm_destroy(W.own_comm);
     }
     delete p;
 }
@@ -585,6 +673,7 @@ llrl_status llrl_comm_create(int device, llrl_comm **out) {
     if (e == cudaSuccess) e = cudaMemset(c->flags, 0, kCommBytes);
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "llrl_comm_create"); }
     c->peer_flags[device] = c->flags;
+    c->nv_next = kNvTableOffset;
     *out = c;
     return LLRL_OK;
 }

@@ -24,6 +24,7 @@ F32, BF16, FP8_E4M3, MXFP8, MXFP4, NVFP4 = 0, 1, 2, 3, 4, 5
 DTYPES = {"f32": F32, "bf16": BF16, "fp8": FP8_E4M3, "mxfp8": MXFP8, "mxfp4": MXFP4, "nvfp4": NVFP4}
 MESH_FSDP_INNER = 1
 PLAN_MULTICAST = 1
+PLAN_NCCL = 2
 (P_ATTN_NORM, P_Q, P_K, P_V, P_O, P_MLP_NORM, P_GATE, P_UP, P_DOWN, P_EMBED, P_FINAL_NORM, P_LM_HEAD,
  P_QKV, P_GATE_UP) = range(14)
 
@@ -34,7 +35,9 @@ EXPORTS = [
     "llrl_plan_device_bytes", "llrl_plan_device_info", "llrl_comm_create", "llrl_comm_export", "llrl_comm_import", "llrl_comm_flag_ptr",
     "llrl_comm_set_peer", "llrl_comm_timed_out", "llrl_comm_destroy", "llrl_ipc_handle", "llrl_ipc_open", "llrl_ipc_close",
     "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_plan_group_range", "llrl_plan_set_max_ctas", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
-    "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error",
+    "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error", "llrl_plan_nv_num_tensors",
+    "llrl_plan_nv_tensor", "llrl_plan_nv_tensor_sources", "llrl_sync_nv_amax", "llrl_nccl_unique_id",
+    "llrl_nccl_attach", "llrl_plan_nccl_info",
     "llrl_version",
 ]
 
@@ -80,7 +83,23 @@ class PlanStats(ctypes.Structure):
 class DeviceInfo(ctypes.Structure):
     _fields_ = [("n_items", ctypes.c_int64), ("n_cast_items", ctypes.c_int64), ("n_fp8_items", ctypes.c_int64),
                 ("n_fp8_pull_items", ctypes.c_int64), ("n_signal", ctypes.c_int32),
-                ("n_senders_in", ctypes.c_int32), ("n_launches", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("n_senders_in", ctypes.c_int32), ("n_launches", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("nv_amax_read_bytes", ctypes.c_int64)]
+
+
+class NcclInfo(ctypes.Structure):
+    _fields_ = [("n_broadcasts", ctypes.c_int32), ("n_allgathers", ctypes.c_int32), ("bytes", ctypes.c_int64),
+                ("mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class NvTensor(ctypes.Structure):
+    _fields_ = [("dst_rank", ctypes.c_int32), ("dst_param", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("n_sources", ctypes.c_int32)]
+
+
+class NvSource(ctypes.Structure):
+    _fields_ = [("src_rank", ctypes.c_int32), ("src_param", ctypes.c_int32), ("src_off", ctypes.c_int64),
+                ("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("src_ld", ctypes.c_int64)]
 
 
 _vp, _i64, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
@@ -129,6 +148,13 @@ _sig("llrl_plan_group_range", [_vp, _int, _int, _int, _P(_i64), _P(_i64)])
 _sig("llrl_sync_group", [_vp, _vp, _int, _int, _P(_vp), _P(_vp), _vp])
 _sig("llrl_sync_host", [_vp, _vp, _int, _P(_vp), _P(_vp), _P(_vp), _P(_vp), _vp])
 _sig("llrl_sync_num_launches", [_vp, _int, _P(_int)])
+_sig("llrl_plan_nv_num_tensors", [_vp, _P(_int)])
+_sig("llrl_plan_nv_tensor", [_vp, _int, _P(NvTensor)])
+_sig("llrl_plan_nv_tensor_sources", [_vp, _int, _int, _int, _P(NvSource)])
+_sig("llrl_sync_nv_amax", [_vp, _vp, _int, _vp, _P(_vp), _P(_vp), _vp])
+_sig("llrl_nccl_unique_id", [ctypes.c_char_p])
+_sig("llrl_nccl_attach", [_vp, _int, ctypes.c_char_p, _int, _int])
+_sig("llrl_plan_nccl_info", [_vp, _int, _P(NcclInfo)])
 _sig("llrl_fill_synthetic", [_vp, _int, _vp, ctypes.c_uint64, _vp])
 _sig("llrl_last_error", [], ctypes.c_char_p)
 _sig("llrl_version", [], ctypes.c_char_p)
@@ -182,6 +208,13 @@ class Layout:
     __del__ = close
 
 
+def nccl_unique_id() -> bytes:
+    """llrl_nccl_unique_id: 128 bytes to share with every process before llrl_nccl_attach."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.llrl_nccl_unique_id(buf))
+    return buf.raw
+
+
 def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", fsdp_inner=False, dp_gen=1,
              pp_train=1, pp_gen=1):
     """llrl_layout_describe_ex -> (src Layout, dst Layout)."""
@@ -197,12 +230,13 @@ def describe(model, fsdp, tp_train, tp_gen, src_dtype="f32", dst_dtype="bf16", f
 class Plan:
     _h = None
 
-    def __init__(self, src: Layout, dst: Layout, src_device, dst_device, multicast=False):
+    def __init__(self, src: Layout, dst: Layout, src_device, dst_device, multicast=False, nccl=False):
         assert len(src_device) == src.n_ranks and len(dst_device) == dst.n_ranks
         h = _vp()
         sd = (_int * len(src_device))(*src_device)
         dd = (_int * len(dst_device))(*dst_device)
-        _check(_lib.llrl_plan_create(src.handle, dst.handle, sd, dd, PLAN_MULTICAST if multicast else 0,
+        _check(_lib.llrl_plan_create(src.handle, dst.handle, sd, dd,
+                                     (PLAN_MULTICAST if multicast else 0) | (PLAN_NCCL if nccl else 0),
                                      ctypes.byref(h)))
         self._h = h
         self.n_src, self.n_dst = src.n_ranks, dst.n_ranks
@@ -279,6 +313,36 @@ class Plan:
         """llrl_sync_group: this device's share of one layer group."""
         _check(_lib.llrl_sync_group(self._h, comm.handle if comm else None, device, group, _ptrs(src_ptrs),
                                     _ptrs(dst_ptrs), _vp(stream)))
+
+    def nv_num_tensors(self):
+        n = _int()
+        _check(_lib.llrl_plan_nv_num_tensors(self._h, ctypes.byref(n)))
+        return n.value
+
+    def nv_tensor(self, tid) -> NvTensor:
+        t = NvTensor()
+        _check(_lib.llrl_plan_nv_tensor(self._h, tid, ctypes.byref(t)))
+        return t
+
+    def nv_tensor_sources(self, tid):
+        n = self.nv_tensor(tid).n_sources
+        out = (NvSource * max(1, n))()
+        _check(_lib.llrl_plan_nv_tensor_sources(self._h, tid, 0, n, out))
+        return list(out[:n])
+
+    def nccl_info(self, device) -> NcclInfo:
+        v = NcclInfo()
+        _check(_lib.llrl_plan_nccl_info(self._h, device, ctypes.byref(v)))
+        return v
+
+    def nccl_attach(self, device, uid: bytes, rank, nranks):
+        """llrl_nccl_attach (collective over every process of the job)."""
+        _check(_lib.llrl_nccl_attach(self._h, device, uid, rank, nranks))
+
+    def sync_nv_amax(self, comm, device, amax_ptr, src_ptrs, dst_ptrs, stream):
+        """llrl_sync_nv_amax: NVFP4 in one pass with the caller's per-tensor amax."""
+        _check(_lib.llrl_sync_nv_amax(self._h, comm.handle if comm else None, device, _vp(amax_ptr),
+                                      _ptrs(src_ptrs), _ptrs(dst_ptrs), _vp(stream)))
 
     def sync_host(self, comm, device, host_src, host_dst, src_ptrs, dst_ptrs, stream):
         _check(_lib.llrl_sync_host(self._h, comm.handle if comm else None, device, _ptrs(host_src),

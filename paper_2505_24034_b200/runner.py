@@ -62,23 +62,18 @@ class SyncJob:
         self.S, self.D = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype,
                                        cfg.dst_dtype, cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
         self.src_dev, self.dst_dev = placement(cfg, spec.n_gpus)
-        # generator DP replicas as a plain replication.  "push" (and
-        # multicast) write every replica from the trainer shards in the fused kernels;
-        # "nccl" fills replica 0 with them and NCCL-broadcasts it to the others.
+        # plain replication.  "push" (and multicast) write every
+        # generator replica from the trainer shards in the fused kernels; "nccl" makes
+        # an LLRL_PLAN_NCCL plan: the library replaces replica copies by ncclBroadcast
+        # or the whole sync by ncclAllGathers where the mapping is a plain
+        # replication (DESIGN R17, R18), all inside llrl_sync.
         if replicate not in ("push", "nccl"):
             raise ValueError(f"replicate must be 'push' or 'nccl', not {replicate!r}")
+        if replicate == "nccl" and multicast:
+            raise ValueError("replicate='nccl' and multicast are exclusive")
         self.replicate = replicate
-        self._bcast = []
-        if replicate == "nccl":
-            if multicast or cfg.dp_gen < 2:
-                raise ValueError("replicate='nccl' needs dp_gen >= 2 and no multicast")
-            ns = self.D.n_ranks // cfg.dp_gen
-            self.bcast_plan = broadcast_plan(self.dst_dev, cfg.dp_gen)
-            self.D0 = llrl.describe(self.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype,
-                                    cfg.fsdp_inner, 1, cfg.pp_train, cfg.pp_gen)[1]
-            self.plan = llrl.Plan(self.S, self.D0, self.src_dev, self.dst_dev[:ns])
-        else:
-            self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev, multicast=multicast)
+        self.plan = llrl.Plan(self.S, self.D, self.src_dev, self.dst_dev, multicast=multicast,
+                              nccl=replicate == "nccl")
         dev = torch.device("cuda", self.device)
         self.src = {r: torch.empty(self.S.rank_bytes(r), dtype=torch.uint8, device=dev)
                     for r in range(self.S.n_ranks) if self.src_dev[r] == self.device}
@@ -112,10 +107,10 @@ class SyncJob:
             self.front = other
         if self.world > 1:
             self._exchange()
-            if replicate == "nccl":
-                self._bcast = make_broadcast_groups(_dist(), self.bcast_plan)
-        elif replicate == "nccl":
-            raise ValueError("replicate='nccl' needs one process per GPU")
+            if self.plan.nccl_info(0).mode:       # llrl_nccl_attach: collective over every process
+                holder = [llrl.nccl_unique_id() if self.rank == 0 else None]
+                _dist().broadcast_object_list(holder, src=0)
+                self.plan.nccl_attach(self.device, holder[0], self.rank, self.world)
         elif cfg.dst_dtype == "nvfp4":
             self.comm = llrl.Comm(self.device)     # NVFP4 keeps its amax table in the comm buffer
 
@@ -243,15 +238,17 @@ class SyncJob:
     # -- the hot path ----------------------------------------------------------
     def sync(self, stream=None):
         s = stream if stream is not None else self.stream
-        if self.replicate == "nccl":
-            ns = self.plan.n_dst
-            if self._in_plan():          # a GPU holding only replicas 1.. has no fused work
-                self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs[:ns], s.cuda_stream)
-            with torch.cuda.stream(s):
-                run_broadcasts(_dist(), self._bcast, self.device, self.dst)
-            return
         if self._in_plan():              # a GPU without trainer or generator ranks has no work
             self.plan.sync(self.comm, self.device, self.src_ptrs, self.dst_ptrs, s.cuda_stream)
+
+    def sync_nv_amax(self, amax, stream=None):
+        """llrl_sync_nv_amax: an NVFP4 sync in one pass with the caller's per-tensor
+        amax (a float32 CUDA tensor on this device, one value per plan tensor id)."""
+        s = stream if stream is not None else self.stream
+        assert amax.dtype == torch.float32 and amax.is_cuda and amax.numel() >= self.plan.nv_num_tensors()
+        if self._in_plan():
+            self.plan.sync_nv_amax(self.comm, self.device, amax.data_ptr(), self.src_ptrs, self.dst_ptrs,
+                                   s.cuda_stream)
 
     def sync_group(self, group, stream=None):
         s = stream if stream is not None else self.stream
@@ -273,6 +270,13 @@ class SyncJob:
         updates group g while llrl_sync_group streams group g-1 out: the sync of a
         layer starts as soon as that layer's update is done."""
         s = stream if stream is not None else self.stream
+        if self.world > 1 and self.plan.stats().n_fp8_pull_blocks:
+            # multi-source fp8 blocks are PULLED from peers' trainer buffers: group g's
+            # pull would only be ordered after the LOCAL optimizer event, so a peer's
+            # half-updated (or next-step) weights could be read.  Refused rather than
+            # racing; llrl_sync_host orders pulls with "staged" handshakes instead.
+            raise ValueError("overlapped_step: the plan pulls fp8 blocks from peer GPUs (uneven FSDP chunks); "
+                             "use sync() after the optimizer step, or sync_host")
         n = self.plan.num_groups()
         opt_stream.wait_stream(s)
         for g in range(n):
@@ -351,47 +355,6 @@ def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener, extra=None):
                     bases[h] = opener(h)
                 ptrs[int(r)] = bases[h] + off
     return flags
-
-
-def broadcast_plan(dst_dev, dp):
-    """NCCL replication of generator DP replicas: for every rank
-    position pos of a replica (R12 numbering q = d*ns + pos), the broadcast from
-    replica 0's GPU to the GPUs of replicas 1..dp-1.  Returns [(pos, root GPU,
-    sorted GPUs, {GPU: generator rank})].  Replicas of one position must sit on
-    pairwise different GPUs (one process per GPU).  Pure host logic."""
-    n = len(dst_dev)
-    if dp < 2 or n % dp:
-        raise ValueError("broadcast_plan: need dp >= 2 dividing the generator ranks")
-    ns = n // dp
-    out = []
-    for pos in range(ns):
-        devs = [dst_dev[d * ns + pos] for d in range(dp)]
-        if len(set(devs)) != dp:
-            raise ValueError(f"broadcast_plan: replicas of generator position {pos} share a GPU ({devs})")
-        out.append((pos, devs[0], sorted(devs), {dev: d * ns + pos for d, dev in enumerate(devs)}))
-    return out
-
-
-def make_broadcast_groups(dist, bplan):
-    """One process group per distinct GPU set (created collectively, same order
-    on every process); process rank == GPU ordinal.  [(root, group, {GPU: q})]."""
-    cache = {}
-    out = []
-    for pos, root, devs, ranks in bplan:
-        key = tuple(devs)
-        if key not in cache:
-            cache[key] = dist.new_group(list(key))
-        out.append((root, cache[key], ranks))
-    return out
-
-
-def run_broadcasts(dist, groups, my_dev, bufs):
-    """Enqueue the replica broadcasts this process takes part in (stream-ordered
-    after the sync that filled replica 0 on the root)."""
-    for root, grp, ranks in groups:
-        q = ranks.get(my_dev)
-        if q is not None:
-            dist.broadcast(bufs[q], src=root, group=grp)
 
 
 def spec_for(name: str, n_gpus: int) -> JobSpec:

@@ -7,7 +7,8 @@ tests/test_gpu_multi.py as
 Each rank owns the trainer / generator ranks placed on its GPU, maps its
 peers' buffers over IPC, runs llrl_sync (push over NVLink + completion flags)
 and compares every generator buffer it owns with the CPU oracle, byte for byte
-(toy), or by oracle point checks (full C2 / C3 sizes with --full).
+(toy and, with --full, every full-size config: streamed per generator
+parameter, tests/harness.py).
 """
 from __future__ import annotations
 
@@ -100,10 +101,16 @@ def toy_case(runner, world, fsdp, tpt, tpg, sdt, ddt, placement, inner=False, se
     job.close()
 
 
-def nccl_replica_case(runner, world, fsdp, tpt, tpg, sdt, ddt, dp, seed=21):
-    """a5: replica 0 filled by the fused kernels, replicas 1.. by NCCL broadcast."""
+def nccl_replica_case(runner, world, fsdp, tpt, tpg, sdt, ddt, dp, seed=21, mode=1):
+    """a5 through llrl_sync on an LLRL_PLAN_NCCL plan: mode 1 = replica 0 by the
+    fused kernels, replicas 1.. by ncclBroadcast (R17); mode 2 = FSDP chunks
+    ncclAllGather-ed into every replica, no kernel of ours (R18)."""
     cfg = LayoutConfig("mp", "toy", fsdp, tpt, tpg, sdt, ddt, "colocated", dp_gen=dp)
     job = runner.SyncJob(runner.JobSpec(cfg, world), fill=False, replicate="nccl")
+    info = job.plan.nccl_info(job.device)
+    assert info.mode == mode, (cfg, info.mode)
+    if mode == 2:
+        assert job.plan.stats().n_items == 0 and info.n_allgathers > 0
     ol = oracle.Layout(job.model, fsdp, tpt, tpg, sdt, ddt, False, dp)
     for rep in range(2):
         src = harness.host_src(ol, seed + rep)
@@ -241,18 +248,43 @@ def random_cases(runner, world, n=24, seed=2505):
 
 
 def full_case(runner, world, name):
-    from tests.test_gpu_parity import _sampled_check
+    """Every byte of every generator buffer of a full-size config at `world`
+    GPUs (tests/harness.py streamed compare): each process fills its own
+    trainer ranks at the oracle's offsets; generator params are dealt out
+    round-robin to the processes, each of which runs the oracle for its params
+    and compares ALL generator ranks' bytes of them (peer buffers read through
+    their IPC mappings); write coverage is summed over processes."""
+    from paper_2505_24034_b200.runner import _wrap_device_ptr
     spec = runner.spec_for(name, world)
-    job = runner.SyncJob(spec, seed=0)
-    for t in job.dst.values():
-        t.fill_(0xFF)
-    torch.cuda.synchronize()
-    dist.barrier()
-    for _ in range(3):
+    job = runner.SyncJob(spec, seed=0, fill=False)
+    cfg = job.cfg
+    ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,
+                       cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+    harness.fill_src_device(ol, 0, job.src)
+    dev = torch.device("cuda", job.device)
+    s_a, s_b = 0xA5, 0x5A
+    counts = []
+    for s in (s_b, s_a):
+        for t in job.dst.values():
+            t.fill_(s)
+        torch.cuda.synchronize()
+        dist.barrier()
         job.sync()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if s == s_b:
+            counts = {q: harness.count_equal(t, s_b) for q, t in job.dst.items()}
+    every = {q: job.dst[q] if q in job.dst else _wrap_device_ptr(job.dst_ptrs[q], job.D.rank_bytes(q), dev)
+             for q in range(job.D.n_ranks)}
+    mine = [gp for gp in range(ol.n_dst_params) if gp % world == dist.get_rank()]
+    workers = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+    n_eq_b = harness.streamed_compare(ol, 0, every, s_a, count_sentinel=s_b, workers=workers, gps=mine)
+    tot = torch.tensor([n_eq_b[q] for q in range(job.D.n_ranks)], dtype=torch.int64, device=dev)
+    dist.all_reduce(tot)
+    for q, c in counts.items():
+        pad = harness.dst_partition(ol, q)[1]
+        assert c == int(tot[q]) + pad, f"{name}: generator rank {q}: {c - int(tot[q]) - pad} byte(s) not written"
     dist.barrier()
-    _sampled_check(job, n_samples=4000, n_blocks=3)
     job.close()
 
 
@@ -306,6 +338,8 @@ def main():
     double_buffer_case(runner, world, 2, 2, 8, "bf16", "fp8", "rotated")
     nccl_replica_case(runner, world, 2, 1, 1, "f32", "bf16", world)       # a5 NCCL replication
     nccl_replica_case(runner, world, 2, 2, 2, "bf16", "fp8", world)
+    nccl_replica_case(runner, world, world, 1, 1, "bf16", "bf16", world, mode=2)   # a5 all-gather
+    nccl_replica_case(runner, world, world, 1, 1, "f32", "f32", world, mode=2)
     if rank0():
         print("ok nccl replicas", flush=True)
     if "--full" in sys.argv:

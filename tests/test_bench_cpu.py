@@ -39,3 +39,31 @@ def test_our_arm_fails_without_cuda():
     r = _run(["--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"])
     assert r.returncode != 0
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")], "printed a number without a GPU"
+
+
+def test_reference_arm_whole_workload_and_same_config():
+    """The reference arm times the whole workload each step (no extrapolation),
+    parameter-parallel over every host core, and reports the same `config`
+    object as our arm (bench.config_dict of the same arguments)."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import CONFIGS
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3"])
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    args = argparse.Namespace(gpus=1, max_ctas=0, multicast=False, replicate="push", step_sync=False,
+                              placement=None)
+    cfg = CONFIGS["c1"]
+    assert d["config"] == bench.config_dict(cfg, args, bench._model_for(cfg, 1))
+    cb = d["cpu_baseline"]
+    assert cb["cores"] == os.cpu_count() and "no extrapolation" in cb["sample"]
+    assert "extrapolat" not in cb["sample"].replace("no extrapolation", "")
+
+
+def test_cpu_baseline_times_the_whole_workload():
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import CONFIGS
+    out = bench.cpu_baseline(CONFIGS["c1"], 1)
+    assert out["cores"] == os.cpu_count() and out["value"] > 0 and out["single_thread_ms"] > 0
+    assert out["nproc"] == os.cpu_count() and out["cpu_model"]

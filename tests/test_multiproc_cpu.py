@@ -76,26 +76,41 @@ def _worker(rank, world, port, q):
                 if dd[g] != rank:
                     assert dst_ptrs[g] == 10 ** 9 * (dd[g] + 1) + 5000 + 1000 * g
                     assert dst1[g] == dst_ptrs[g] + 500
-        # a5 NCCL-style replica broadcast (runner.broadcast_plan / run_broadcasts) on gloo:
-        # replica 0's buffers reach every replica, other ranks' buffers stay untouched
-        import torch
-        for dp, ns in ((world, 1), (world, 2), (2, 3)):
-            n = dp * ns
-            dd = [(d + pos) % world if dp == world else (pos + d * (world // 2)) % world
-                  for d in range(dp) for pos in range(ns)]
-            bp = runner.broadcast_plan(dd, dp)
-            assert [b[0] for b in bp] == list(range(ns))
-            assert all(b[1] == dd[b[0]] and len(b[2]) == dp for b in bp)
-            groups = runner.make_broadcast_groups(dist, bp)
-            bufs = {qq: torch.full((64,), -1.0) for qq in range(n) if dd[qq] == rank}
-            for qq in bufs:
-                if qq < ns:                       # replica 0 holds the synced bytes
-                    bufs[qq] = torch.arange(64, dtype=torch.float32) + 100 * qq
-            runner.run_broadcasts(dist, groups, rank, bufs)
-            for qq, t in bufs.items():
-                assert torch.equal(t, torch.arange(64, dtype=torch.float32) + 100 * (qq % ns)), (dp, ns, qq)
-        with pytest.raises(ValueError):
-            runner.broadcast_plan([0, 0], 2)      # replicas of one position on one GPU
+        # a5 (LLRL_PLAN_NCCL): every rank derives the same NCCL operations from the
+        # plan (a collective must be entered identically everywhere), and the
+        # replicated bytes match the layouts
+        from synth import LayoutConfig
+        for cfg in (LayoutConfig("b", "llama3-8b", 2, 1, 1, "bf16", "bf16", "disjoint", dp_gen=world),
+                    LayoutConfig("b", "toy", 3, 1, 2, "f32", "bf16", "disjoint", dp_gen=world),
+                    LayoutConfig("g", "llama3-8b", world, 1, 1, "bf16", "bf16", "colocated", dp_gen=world),
+                    LayoutConfig("g", "toy", world, 1, 1, "f32", "f32", "colocated", dp_gen=world)):
+            m = MODELS[cfg.model]
+            S, D = llrl.describe(m, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, False,
+                                 cfg.dp_gen)
+            sd = [r * world // cfg.n_src for r in range(cfg.n_src)] if cfg.placement == "colocated" else [0] * cfg.n_src
+            ns = D.n_ranks // cfg.dp_gen
+            dd = ([q % world for q in range(D.n_ranks)] if cfg.placement == "colocated" else
+                  [(q // ns) % world for q in range(D.n_ranks)])
+            plan = llrl.Plan(S, D, sd, dd, nccl=True)
+            infos = [(i.mode, i.n_broadcasts, i.n_allgathers, i.bytes)
+                     for i in (plan.nccl_info(d) for d in range(plan.stats().n_devices))]
+            allinfo = [None] * world
+            dist.all_gather_object(allinfo, infos)
+            assert all(a == infos for a in allinfo), "ranks derived different NCCL operations"
+            if cfg.name == "g":                  # FSDP chunks all-gathered: no kernel work at all
+                assert all(i[0] == 2 for i in infos) and plan.stats().n_items == 0
+                data = sum(D.param_view(0, gp).rows * D.param_view(0, gp).cols for gp in range(D.n_params))
+                es = 4 if cfg.src_dtype == "f32" else 2
+                assert all(i[3] == data * es * (world - 1) // world for i in infos)
+            else:                                # replicas 1.. by broadcast of replica 0's buffer
+                assert all(i[0] == 1 for i in infos)
+                for d, i in enumerate(infos):
+                    reps = [q for q in range(ns, D.n_ranks) if dd[q] == d]
+                    assert i[3] == sum(D.rank_bytes(q) for q in reps)
+                    assert i[1] == len({q % ns for q in range(D.n_ranks) if dd[q] == d})
+                # the kernels write replica 0 only
+                runs = plan.runs()
+                assert runs.size and int(runs["dst_rank"].max()) < ns
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))

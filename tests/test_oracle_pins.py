@@ -483,3 +483,88 @@ def test_oracle_generator_shards_concatenate_to_cast_full(oracle_lib, fsdp, tpt,
 def harness_oracle_dst(ol, seed):
     from tests import harness
     return harness.oracle_dst(ol, harness.host_src(ol, seed))
+
+
+# --------------------------------------------------------------------------- point-check helpers
+
+def _id_tensors(m):
+    """Full tensors whose element bits are a global element id (param-major,
+    row-major): decoding a generator element's bits gives its source coordinate."""
+    full, starts, shapes = {}, [], []
+    base = 0
+    for pid, (name, R, C, split) in enumerate(brute.src_params(m)):
+        full[name] = (np.arange(R * C, dtype=np.uint64) + np.uint64(base)).astype(np.uint32).reshape(R, C)
+        starts.append(base)
+        shapes.append((R, C))
+        base += R * C
+    assert base < 2 ** 32
+    return full, np.array(starts, np.int64), shapes
+
+
+def _decode_ids(ids, starts, shapes):
+    pid = np.searchsorted(starts, ids.astype(np.int64), side="right") - 1
+    cols = np.array([c for _, c in shapes], np.int64)[pid]
+    loc = ids.astype(np.int64) - starts[pid]
+    return pid, loc // cols, loc % cols
+
+
+ELEM_SRC_CASES = ([(f, tt, tg, 1, 1, 1, False) for f in (1, 2, 3, 4, 8) for tt in (1, 2, 4, 8) for tg in (1, 2, 4, 8)]
+                  + [(2, 2, 8, 1, 1, 1, True), (3, 1, 4, 3, 1, 1, False), (2, 1, 2, 1, 2, 1, False),
+                     (1, 2, 2, 1, 1, 2, False), (3, 1, 4, 2, 2, 2, False)])
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,dp,ppt,ppg,inner", ELEM_SRC_CASES)
+def test_dst_element_source_vs_brute(oracle_lib, fsdp, tpt, tpg, dp, ppt, ppg, inner):
+    """orc_dst_element_source (the index map every full-size point check relies
+    on), for EVERY element of every generator param of every rank, against the
+    independent brute force: tensors whose bits are their own global element id,
+    re-split by brute.generator_pieces (torch.chunk / np.concatenate, readings
+    R4, R12, R14) in identity (f32) mode, then decoded."""
+    m = MODELS["toy"]
+    full, starts, shapes = _id_tensors(m)
+    ranks = brute.generator_pieces(m, full, tpg, "f32", "f32", ppg, grouped=True)
+    L = oracle.Layout(m, fsdp, tpt, tpg, "f32", "f32", inner, dp, ppt, ppg)
+    assert L.status == 0
+    for q in range(L.n_dst):
+        tensors = ranks[q % (tpg * ppg)]
+        assert len(tensors) == L.n_dst_params
+        for gp in range(L.n_dst_params):
+            want = tensors[gp][0].view(np.uint32)
+            R, C = L.dst_param(q, gp)[:2]
+            assert want.size == R * C, (q, gp)
+            if R * C == 0:
+                continue
+            p, r, c = L.dst_param_sources(q, gp)
+            wp, wr, wc = _decode_ids(want.reshape(R, C), starts, shapes)
+            assert np.array_equal(p, wp) and np.array_equal(r, wr) and np.array_equal(c, wc), (q, gp)
+            # the scalar entry point agrees with the vector one on the corners
+            for lr, lc in ((0, 0), (R - 1, C - 1), (R // 2, C // 3)):
+                assert L.dst_element_source(q, gp, lr, lc) == (p[lr, lc], r[lr, lc], c[lr, lc])
+
+
+@pytest.mark.parametrize("fsdp,tpt,tpg,sdt,ddt,dp,ppg", [
+    (2, 1, 2, "f32", "nvfp4", 1, 1), (2, 2, 8, "bf16", "nvfp4", 1, 1), (3, 1, 4, "bf16", "nvfp4", 2, 1),
+    (1, 2, 2, "bf16", "nvfp4", 1, 2), (3, 1, 4, "f32", "fp8", 1, 1), (2, 2, 8, "bf16", "mxfp8", 1, 1),
+    (3, 1, 4, "f32", "mxfp4", 1, 2), (2, 1, 2, "f32", "bf16", 1, 1)])
+def test_dst_offsets_vs_brute_packing(oracle_lib, fsdp, tpt, tpg, sdt, ddt, dp, ppg):
+    """orc_dst_param's data / scale-grid offsets and orc_dst_tensor_scale_off (the
+    NVFP4 fp32 tensor scale every full-size check reads) against brute.py's own
+    walk of the generator tensors (reading R0, R9, R16): codes, scale grid and
+    tensor scale each at the next 256-byte boundary."""
+    m = MODELS["toy"]
+    full = brute.full_tensors(m, 3, sdt)
+    ranks = brute.generator_pieces(m, full, tpg, sdt, ddt, ppg, grouped=True)
+    L = oracle.Layout(m, fsdp, tpt, tpg, sdt, ddt, False, dp, 1, ppg)
+    assert L.status == 0
+    for q in range(L.n_dst):
+        tensors = ranks[q % (tpg * ppg)]
+        offs, total = brute.offsets([a for grp in tensors for a in grp])
+        assert L.dst_rank_bytes(q) == total
+        k = 0
+        for gp, grp in enumerate(tensors):
+            R, C, quant, off, soff = L.dst_param(q, gp)
+            assert off == offs[k], (q, gp)
+            assert quant == (len(grp) > 1)
+            assert soff == (offs[k + 1] if len(grp) > 1 else -1), (q, gp)
+            assert L.dst_tensor_scale_off(q, gp) == (offs[k + 2] if len(grp) == 3 else -1), (q, gp)
+            k += len(grp)
