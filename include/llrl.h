@@ -386,6 +386,12 @@ llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n);
 llrl_status llrl_fill_synthetic(const llrl_layout *src, int rank, void *dev_ptr, uint64_t seed,
                                 void *stream);
 
+/* Debug timeline (set LLRL_TIMELINE=1 before the plan's first sync on `device`):
+ * out[2c], out[2c+1] = %globaltimer (ns) when CTA c of the last cast launch
+ * started / finished its last store; *n_ctas = CTAs copied (0 when disabled).
+ * Synchronous. */
+llrl_status llrl_debug_timeline(const llrl_plan *p, int device, uint64_t *out, int max_ctas, int *n_ctas);
+
 const char *llrl_last_error(void);
 const char *llrl_version(void);
 

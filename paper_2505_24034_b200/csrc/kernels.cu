@@ -424,7 +424,20 @@ __device__ void fp8_item_generic(const Item &it, const KParams &P, uint32_t *s_r
 // waits for the cast grid's completion before it completes or signals.
 __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Debug timeline (LLRL_TIMELINE=1): %globaltimer at CTA start / after its last
+// store, per CTA of the cast launch (llrl_debug_timeline).
+__device__ __forceinline__ void timeline_mark(const KParams &P, int which) {
+    if (P.timeline == nullptr) return;
+    if (which) __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.timeline[2 * blockIdx.x + which] = t;
+    }
+}
+
 __device__ __forceinline__ void complete(const KParams &P) {
+    timeline_mark(P, 1);
     if (P.pdl_wait) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
@@ -446,6 +459,7 @@ __device__ __forceinline__ void complete(const KParams &P) {
 template <bool SRC_F32, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) llrl_k_cast(const __grid_constant__ KParams P) {
     pdl_release();
+    timeline_mark(P, 0);
     for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
         const Item it = P.items[i];
         cast_item<SRC_F32, U>(it, P);
@@ -649,6 +663,7 @@ template <bool SRC_F32, int SB, int NST, int NWK, int MINB>
 __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_constant__ KParams P) {
     constexpr int kCastStageBytes = SB, kCastStages = NST, kCastWorkers = NWK;
     pdl_release();
+    timeline_mark(P, 0);
     // warp 0: producer (bulk loads global -> shared), warp 1: storer (bulk stores
     // shared -> global), warps 2..: workers (conversion in shared memory).  A stage
     // moves full (producer -> workers) -> converted (workers -> storer) -> empty

@@ -24,6 +24,7 @@ struct KParams {
     const void *src[kMaxRanks];
     void *dst[kMaxRanks];
     void *dst_mc[kMaxRanks];           // multicast VA per dst rank (F_MC items)
+    unsigned long long *timeline;      // debug (LLRL_TIMELINE): [grid][start, end] of the cast launch, or null
     int pdl_wait;                      // launched as a programmatic dependent of the previous
                                        // launch: wait for it before completing / signalling
 };

@@ -55,6 +55,26 @@ struct Builder {
         return true;
     }
     std::vector<std::vector<std::vector<int>>> mc_extra;   // [exec dev][group] -> replica devices to signal
+    uint64_t mc_counter = 0;
+    // elements per cast item: chunk_elems(), or 4 Ki for tiny syncs (< 64 MB of
+    // cast source in the plan: latency-bound, so more CTAs each with one short
+    // dependent round trip beat fewer longer ones)
+    int64_t chunk = chunk_elems();
+    void size_chunks() {
+        if (getenv("LLRL_CHUNK_ELEMS")) return;
+        int64_t bytes = 0;
+        for (const Tile &t : P->tiles) bytes += t.rows * t.cols * es_src;
+        if (bytes < (int64_t(64) << 20)) chunk = 4096;
+    }
+    // multicast egress split: every k-th multicast item is pushed to each replica
+    // instead (0 = all multicast); LLRL_MC_UNICAST_PERIOD overrides (tuning knob)
+    static int mc_unicast_period() {
+        static const int k = [] {
+            const char *v = getenv("LLRL_MC_UNICAST_PERIOD");
+            return v ? std::max(0, atoi(v)) : 9;
+        }();
+        return k;
+    }
 
     // a5 broadcast (R17): replica d >= 1 of a rank position whose replicas sit on
     // pairwise different GPUs is a byte copy of replica 0 -- left to ncclBroadcast.
@@ -224,10 +244,10 @@ struct Builder {
             // one 1-D run: scalar head up to a 16-byte destination boundary, vector body, scalar tail
             int64_t n = t.rows * t.cols, so = t.src_off, dof = t.dst_off;
             auto emit = [&](int64_t s, int64_t d, int64_t len, bool vec) {
-                for (int64_t i = 0; i < len; i += chunk_elems()) {
+                for (int64_t i = 0; i < len; i += chunk) {
                     Item it = base;
                     it.src_off = s + i; it.dst_off = d + i;
-                    it.rows = 1; it.cols = int32_t(std::min(chunk_elems(), len - i));
+                    it.rows = 1; it.cols = int32_t(std::min(chunk, len - i));
                     it.src_ld = it.cols; it.dst_ld = it.cols;
                     it.flags = uint8_t(fl | (vec ? F_VEC : 0));
                     out.push_back(it);
@@ -247,7 +267,7 @@ struct Builder {
         }
         const bool vec = (t.src_off % 8 == 0) && (t.dst_off % 8 == 0) && (t.cols % 8 == 0) &&
                          (t.src_ld % 8 == 0) && (t.dst_ld % 8 == 0);
-        const int64_t rows_per = std::max<int64_t>(1, chunk_elems() / t.cols);
+        const int64_t rows_per = std::max<int64_t>(1, chunk / t.cols);
         for (int64_t r = 0; r < t.rows; r += rows_per) {
             Item it = base;
             it.rows = int32_t(std::min(rows_per, t.rows - r));
@@ -418,6 +438,19 @@ struct Builder {
             add_cast_items(t, tmp);
             for (Item it : tmp) {
                 const int64_t n = int64_t(it.rows) * it.cols;
+                // egress split: NVLS multicast stores top out below the link rate
+                // (~560 of ~770 GB/s), so one item in mc_unicast_period() goes to
+                // every replica as plain peer pushes, filling the link's headroom
+                if (mc_unicast_period() > 0 && (mc_counter++ % uint64_t(mc_unicast_period())) == 0) {
+                    for (int d = 0; d < D->dp_gen; d++) {
+                        Item u = it;
+                        u.dst_rank = uint8_t(d * n_pos() + pos);   // replicas share replica 0's layout (R12)
+                        const int rd = P->dst_device[size_t(u.dst_rank)];
+                        lists[sd][rd][grp].push_back(u);
+                        account(sd, sd, rd, n * es_src, n * es_dst, false);
+                    }
+                    continue;
+                }
                 {
                     it.flags = uint8_t(it.flags | F_MC);
                     lists[sd][dd][grp].push_back(it);
@@ -705,7 +738,10 @@ llrl_status llrl_plan_create(const llrl_layout *src, const llrl_layout *dst, con
         P->nccl_mode = b.allgather_eligible() ? 2 : dst->dp_gen >= 2 ? 1 : 0;
     }
     llrl_status st = b.make_tiles();
-    if (st == LLRL_OK) st = b.make_items();
+    if (st == LLRL_OK) {
+        b.size_chunks();
+        st = b.make_items();
+    }
     if (st == LLRL_OK) b.make_nccl_ops();
     if (st == LLRL_OK && P->nccl_mode == 1 && P->nccl_bcast.empty()) P->nccl_mode = 0;
     if (st != LLRL_OK) { delete P; return st; }

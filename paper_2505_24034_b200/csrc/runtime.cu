@@ -124,6 +124,11 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         const int g = int(std::min<int64_t>(cap, std::max<int64_t>(1, n)));
         (mode == 0 ? W.grid_cast : W.grid_fp8) = g;
     }
+    if (const char *v = getenv("LLRL_TIMELINE"))
+        if (atoi(v) && W.grid_cast > 0) {
+            CK(cudaMalloc(&W.d_timeline, size_t(W.grid_cast) * 16));
+            CK(cudaMemset(W.d_timeline, 0, size_t(W.grid_cast) * 16));
+        }
     W.uploaded_device = device;
     return LLRL_OK;
 }
@@ -263,7 +268,7 @@ static void free_device_tables(DeviceWork &W) {
                      reinterpret_cast<void **>(&W.d_tmaps), reinterpret_cast<void **>(&W.d_nv_partial),
                      reinterpret_cast<void **>(&W.d_nv_amax), reinterpret_cast<void **>(&W.d_nv_contrib),
                      reinterpret_cast<void **>(&W.d_nv_tensor_dev), reinterpret_cast<void **>(&W.d_nv_local),
-                     reinterpret_cast<void **>(&W.d_nv_done)};
+                     reinterpret_cast<void **>(&W.d_nv_done), reinterpret_cast<void **>(&W.d_timeline)};
     for (void **q : ptrs) {
         cudaFree(*q);
         *q = nullptr;
@@ -292,6 +297,7 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
             for (int i = 0; i < kp.n_signal; i++) kp.signal[i] = comm->peer_flags[sig[size_t(i)]] + comm->device;
         }
         kp.pdl_wait = (mode == 1 && c1 > c0 && !W.no_pdl) ? 1 : 0;   // fp8 launch overlaps the cast tail
+        kp.timeline = mode == 0 ? W.d_timeline : nullptr;
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
         kp.pdl_wait = 0;
     }
@@ -513,6 +519,18 @@ llrl_status llrl_sync_group(llrl_plan *p, llrl_comm *comm, int device, int group
                        W.group_signal[g], s);
     if (st != LLRL_OK) return st;
     return wait_arrivals(comm, W.group_senders[g], s);
+}
+
+llrl_status llrl_debug_timeline(const llrl_plan *p, int device, uint64_t *out, int max_ctas, int *n_ctas) {
+    if (!p || !out || !n_ctas || device < 0 || device >= p->n_devices) { set_error("invalid argument"); return LLRL_E_INVALID; }
+    const DeviceWork &W = p->dev[size_t(device)];
+    *n_ctas = 0;
+    if (!W.d_timeline) return LLRL_OK;
+    DeviceGuard guard(device);
+    const int n = std::min(max_ctas, W.grid_cast);
+    CK(cudaMemcpy(out, W.d_timeline, size_t(n) * 16, cudaMemcpyDeviceToHost));
+    *n_ctas = n;
+    return LLRL_OK;
 }
 
 llrl_status llrl_sync_num_launches(const llrl_plan *p, int device, int *n) {

@@ -37,7 +37,7 @@ EXPORTS = [
     "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_plan_group_range", "llrl_plan_set_max_ctas", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
     "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error", "llrl_plan_nv_num_tensors",
     "llrl_plan_nv_tensor", "llrl_plan_nv_tensor_sources", "llrl_sync_nv_amax", "llrl_nccl_unique_id",
-    "llrl_nccl_attach", "llrl_plan_nccl_info",
+    "llrl_nccl_attach", "llrl_plan_nccl_info", "llrl_debug_timeline",
     "llrl_version",
 ]
 
@@ -155,6 +155,7 @@ _sig("llrl_sync_nv_amax", [_vp, _vp, _int, _vp, _P(_vp), _P(_vp), _vp])
 _sig("llrl_nccl_unique_id", [ctypes.c_char_p])
 _sig("llrl_nccl_attach", [_vp, _int, ctypes.c_char_p, _int, _int])
 _sig("llrl_plan_nccl_info", [_vp, _int, _P(NcclInfo)])
+_sig("llrl_debug_timeline", [_vp, _int, _P(ctypes.c_uint64), _int, _P(_int)])
 _sig("llrl_fill_synthetic", [_vp, _int, _vp, ctypes.c_uint64, _vp])
 _sig("llrl_last_error", [], ctypes.c_char_p)
 _sig("llrl_version", [], ctypes.c_char_p)
@@ -329,6 +330,14 @@ class Plan:
         out = (NvSource * max(1, n))()
         _check(_lib.llrl_plan_nv_tensor_sources(self._h, tid, 0, n, out))
         return list(out[:n])
+
+    def debug_timeline(self, device, max_ctas=4096):
+        """llrl_debug_timeline: [(start_ns, end_ns)] per CTA of the last cast launch
+        (needs LLRL_TIMELINE=1 before the first sync)."""
+        buf = (ctypes.c_uint64 * (2 * max_ctas))()
+        n = _int()
+        _check(_lib.llrl_debug_timeline(self._h, device, buf, max_ctas, ctypes.byref(n)))
+        return [(buf[2 * c], buf[2 * c + 1]) for c in range(n.value)]
 
     def nccl_info(self, device) -> NcclInfo:
         v = NcclInfo()
