@@ -256,6 +256,11 @@ def full_case(runner, world, name):
     their IPC mappings); write coverage is summed over processes."""
     from paper_2505_24034_b200.runner import _wrap_device_ptr
     spec = runner.spec_for(name, world)
+    # bounded host time: the whole 8B model; 4 decoder layers (+ embed / lm_head)
+    # of 70B and 2 of the 405B slice -- same shapes per layer, same kernels
+    layers = {"llama3-70b": 4, "llama3-405b-slice16": 2}.get(spec.cfg.model)
+    if layers is not None:
+        spec = runner.JobSpec(spec.cfg, world, n_layers=max(layers, spec.cfg.pp_train, spec.cfg.pp_gen))
     job = runner.SyncJob(spec, seed=0, fill=False)
     cfg = job.cfg
     ol = oracle.Layout(job.model, cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype, cfg.fsdp_inner,

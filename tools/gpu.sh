@@ -1,0 +1,89 @@
+#!/usr/bin/env bash
+# tools/gpu.sh -- the measurement recipes run on the GPU box through gpurun
+# (replaces round 1's one-off tools/run_*.sh).  Outputs land in gpurun_out/.
+#
+#   gpurun [--gpus N] -- 'bash tools/gpu.sh <recipe> [args]'
+#
+# recipes
+#   tests [N]            pytest -m gpu on this box (N GPUs visible: the multi-GPU
+#                        parity of tests/test_gpu_multi.py runs at every n <= N)
+#   bench N CFG [extra]  bench.py at N GPUs (torchrun for N > 1), config CFG
+#   table N CFGS...      bench.py --no-e2e for each config at N GPUs
+#   scale [N]            the default bench (C2) at 1, 2, ... N GPUs + reference arm
+#   timeline N CFG       per-CTA start / end spread of the cast launch (tools/timeline.py)
+#   launches CFG         ncu launch list (gpu__time_duration, --clock-control none), 1 GPU
+#   ncufull CFG KERNEL   ncu --set full of one kernel (regex), 1 GPU, 1 launch
+#   nvlink N CFG         ncu NVLink + DRAM counters, one process driving N GPUs
+set -u
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+R="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+port=$((29500 + RANDOM % 400))
+run_bench() {  # N CFG extra...
+    local n=$1 cfg=$2; shift 2
+    port=$((port + 1))
+    if [ "$n" = 1 ]; then
+        timeout 900 python bench.py --config "$cfg" "$@"
+    else
+        timeout 900 $R --nproc-per-node "$n" --master-port $port bench.py --gpus "$n" --config "$cfg" "$@"
+    fi
+}
+recipe=${1:-tests}; shift || true
+case "$recipe" in
+tests)
+    python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+    timeout 3000 python -m pytest tests -m gpu -q -rs --durations=15 > gpurun_out/pytest_gpu.log 2>&1
+    echo "pytest rc=$? ($(git rev-parse --short HEAD 2>/dev/null || echo snapshot))" >> gpurun_out/pytest_gpu.log
+    tail -5 gpurun_out/pytest_gpu.log ;;
+bench)
+    n=$1; cfg=$2; shift 2
+    run_bench "$n" "$cfg" "$@" > "gpurun_out/bench_${cfg}_n${n}.json" 2> "gpurun_out/bench_${cfg}_n${n}.err"
+    tail -c 600 "gpurun_out/bench_${cfg}_n${n}.json" ;;
+table)
+    n=$1; shift
+    for cfg in "$@"; do
+        run_bench "$n" "$cfg" --steps 10 --warmup 3 --no-e2e --no-cpu-baseline \
+            > "gpurun_out/table_${cfg}_n${n}.json" 2> "gpurun_out/table_${cfg}_n${n}.err"
+        python - "$cfg" "$n" <<'EOF'
+import json, sys
+cfg, n = sys.argv[1], sys.argv[2]
+try:
+    d = json.loads(open(f"gpurun_out/table_{cfg}_n{n}.json").read().strip().splitlines()[-1])
+    r = d["roofline"]
+    print(cfg, n, d["value"], r["bound"], r["achieved"], r["frac"], r["t_lb_ms"],
+          d.get("nvfp4_supplied_amax", {}).get("value"))
+except Exception as e:
+    print(cfg, n, "FAILED", e)
+EOF
+    done ;;
+scale)
+    top=${1:-4}
+    timeout 900 python bench.py > gpurun_out/scale_n1.json 2> gpurun_out/scale_n1.err
+    for n in 2 4 8; do
+        [ "$n" -le "$top" ] || break
+        port=$((port + 1))
+        timeout 900 $R --nproc-per-node $n --master-port $port bench.py --gpus $n > gpurun_out/scale_n$n.json 2> gpurun_out/scale_n$n.err
+    done
+    timeout 900 python bench.py --impl reference > gpurun_out/scale_ref_n1.json 2> gpurun_out/scale_ref_n1.err ;;
+timeline)
+    n=$1; cfg=$2; port=$((port + 1))
+    timeout 600 $R --nproc-per-node "$n" --master-port $port tools/timeline.py --gpus "$n" --config "$cfg" \
+        > "gpurun_out/timeline_${cfg}_n${n}.jsonl" 2> "gpurun_out/timeline_${cfg}_n${n}.err" ;;
+launches)
+    cfg=$1
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        --log-file "gpurun_out/launches_${cfg}.csv" python bench.py --config "$cfg" --steps 2 --warmup 3 \
+        --no-e2e --no-cpu-baseline > "gpurun_out/launches_${cfg}.log" 2>&1 ;;
+ncufull)
+    cfg=$1; k=$2
+    timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$k" -c 1 \
+        -o "gpurun_out/ncu_${cfg}_${k}" python bench.py --config "$cfg" --steps 1 --warmup 3 --no-e2e \
+        --no-cpu-baseline --no-nv-supplied > "gpurun_out/ncufull_${cfg}.log" 2>&1 ;;
+nvlink)
+    n=$1; cfg=$2
+    timeout 1500 ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none -k regex:llrl_k_cast --csv --log-file "gpurun_out/nvlink_${cfg}_n${n}.csv" \
+        python tools/nvlink_1proc.py "$cfg" "$n" >"gpurun_out/nvlink_${cfg}_n${n}.log" 2>&1 ;;
+*)
+    echo "unknown recipe $recipe"; exit 2 ;;
+esac
