@@ -205,6 +205,8 @@ struct DeviceWork {
     std::vector<const void *> tmap_src;     // src base pointers the maps were encoded for
     unsigned long long *d_done = nullptr;   // last-CTA counter (cumulative)
     unsigned long long *d_timeline = nullptr;   // LLRL_TIMELINE: per-CTA start / end of the cast launch
+    unsigned int *d_queue = nullptr;            // dynamic item queue of the TMA cast launch
+    bool static_items = false;                  // LLRL_STATIC_ITEMS=1: static striding instead
     void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)
     std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8

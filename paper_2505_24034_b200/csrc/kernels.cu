@@ -438,6 +438,15 @@ __device__ __forceinline__ void timeline_mark(const KParams &P, int which) {
 
 __device__ __forceinline__ void complete(const KParams &P) {
     timeline_mark(P, 1);
+    if (P.queue) {
+        // dynamic item queue (llrl_k_cast_tma): the last CTA out -- every claim
+        // made -- resets it for the next launch (graph-replayable)
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(P.queue + 1, 1u) + 1 == gridDim.x) {
+            atomicExch(P.queue, 0u);
+            atomicExch(P.queue + 1, 0u);
+        }
+    }
     if (P.pdl_wait) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
@@ -685,10 +694,21 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    __shared__ int s_item[kCastStages], s_chunk[kCastStages];   // what each stage holds (-1: end of work)
     if (warp == 0) {
-        // producer: stage rows of every vector item; scalar items pass a token
+        // producer: claims items and stages the rows of every vector item; scalar
+        // items pass a token.  Claims are dynamic (one atomicAdd per item on the
+        // launch's queue, issued one item ahead so its latency hides behind the
+        // current item's copies): CTAs that drew cheap (local) items take more, so
+        // all finish together instead of the last CTA setting the sync's tail
+        // (static striding when P.queue is null).  Each stage carries its item and
+        // chunk in s_item / s_chunk, written before the arrive (release -> acquire).
         int n = 0;
-        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+        unsigned claimed = 0;
+        if (P.queue && lane == 0) claimed = atomicAdd(P.queue, 1u);
+        int i = P.queue ? P.item_begin + int(__shfl_sync(0xffffffffu, claimed, 0)) : P.item_begin + int(blockIdx.x);
+        while (i < P.item_end) {
+            if (P.queue && lane == 0) claimed = atomicAdd(P.queue, 1u);   // the next item, in flight
             const Item it = P.items[i];
             int rows_per, segs;
             const int nch = (it.flags & F_VEC) ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
@@ -696,6 +716,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+                if (lane == 0) {
+                    s_item[st] = i;
+                    s_chunk[st] = k;
+                }
                 if (!(it.flags & F_VEC)) {
                     if (lane == 0) mbar_arrive(&full_bar[st]);
                     continue;
@@ -713,22 +737,29 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                  uint32_t(c.nc * es), &full_bar[st]);
                 }
             }
+            i = P.queue ? P.item_begin + int(__shfl_sync(0xffffffffu, claimed, 0)) : i + int(gridDim.x);
+        }
+        const int st = n % kCastStages;          // end-of-work token
+        mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+        if (lane == 0) {
+            s_item[st] = -1;
+            mbar_arrive(&full_bar[st]);
         }
     } else if (warp == 1) {
         // storer: write each converted stage back, release it once read
-        int n = 0, pend = -1;
-        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+        int pend = -1;
+        for (int n = 0;; n++) {
+            const int st = n % kCastStages;
+            mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
+            const int i = s_item[st];
+            if (i < 0) break;
             const Item it = P.items[i];
-            int rows_per, segs;
             const bool vec = it.flags & F_VEC;
-            const int nch = vec ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
             const int des = mx ? 1 : cast ? 2 : es;
             char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
-            for (int k = 0; k < nch; k++, n++) {
-                const int st = n % kCastStages;
-                mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
+            {
                 if (!vec) {                       // scalar item: workers wrote global memory directly
                     if (lane == 0) {
                         // release the deferred stage now: the producer may need it before
@@ -743,7 +774,9 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                     continue;
                 }
                 if (lane == 0) {
-                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
+                    int rows_per, segs;
+                    cast_chunks<SB>(it, es, &rows_per, &segs);
+                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, s_chunk[st]);
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
                     // rows contiguous in the destination (chunk spans whole rows): one bulk store
                     const int nrow = c.nc == it.dst_ld ? 1 : c.nr, nel = c.nc == it.dst_ld ? c.nr * c.nc : c.nc;
@@ -766,15 +799,20 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
     } else {
         // workers
         const int wt = threadIdx.x - 64;
-        int n = 0;
         int nv_tid = -1, nv_buf = 0;
-        for (int i = P.item_begin + blockIdx.x; i < P.item_end; i += gridDim.x) {
+        for (int n = 0;; n++) {
+            const int st = n % kCastStages;
+            mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+            const int i = s_item[st], k = s_chunk[st];
+            if (i < 0) {                          // end of work: pass the token to the storer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv_bar[st]);
+                break;
+            }
             const Item it = P.items[i];
             const bool dst_f32 = it.flags & F_DST_F32;
             char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
-                const int st = n % kCastStages;
-                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
                 const char *src = static_cast<const char *>(P.src[it.src_rank]);
                 const int ne = it.rows * it.cols;
                 for (int e = wt; e < ne; e += kCastWorkers) {
@@ -791,11 +829,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
-                n++;
                 continue;
             }
             int rows_per, segs;
-            const int nch = cast_chunks<SB>(it, es, &rows_per, &segs);
+            cast_chunks<SB>(it, es, &rows_per, &segs);
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
@@ -815,9 +852,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 if (wt == 0) nv_senc[nv_buf] = s_enc;
                 asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
             }
-            for (int k = 0; k < nch; k++, n++) {
-                const int st = n % kCastStages;
-                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+            {
                 unsigned char *in = stages + st * kStride;
                 unsigned char *out = in + kCastStageBytes;
                 if (cast || mx) {

@@ -25,6 +25,7 @@ struct KParams {
     void *dst[kMaxRanks];
     void *dst_mc[kMaxRanks];           // multicast VA per dst rank (F_MC items)
     unsigned long long *timeline;      // debug (LLRL_TIMELINE): [grid][start, end] of the cast launch, or null
+    unsigned int *queue;               // TMA cast launch: [next item, CTAs done] (dynamic claims), or null
     int pdl_wait;                      // launched as a programmatic dependent of the previous
                                        // launch: wait for it before completing / signalling
 };

@@ -124,6 +124,9 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         const int g = int(std::min<int64_t>(cap, std::max<int64_t>(1, n)));
         (mode == 0 ? W.grid_cast : W.grid_fp8) = g;
     }
+    CK(cudaMalloc(&W.d_queue, 256));
+    CK(cudaMemset(W.d_queue, 0, 256));
+    if (const char *v = getenv("LLRL_STATIC_ITEMS")) W.static_items = atoi(v) != 0;
     if (const char *v = getenv("LLRL_TIMELINE"))
         if (atoi(v) && W.grid_cast > 0) {
             CK(cudaMalloc(&W.d_timeline, size_t(W.grid_cast) * 16));
@@ -268,7 +271,8 @@ static void free_device_tables(DeviceWork &W) {
                      reinterpret_cast<void **>(&W.d_tmaps), reinterpret_cast<void **>(&W.d_nv_partial),
                      reinterpret_cast<void **>(&W.d_nv_amax), reinterpret_cast<void **>(&W.d_nv_contrib),
                      reinterpret_cast<void **>(&W.d_nv_tensor_dev), reinterpret_cast<void **>(&W.d_nv_local),
-                     reinterpret_cast<void **>(&W.d_nv_done), reinterpret_cast<void **>(&W.d_timeline)};
+                     reinterpret_cast<void **>(&W.d_nv_done), reinterpret_cast<void **>(&W.d_timeline),
+                     reinterpret_cast<void **>(&W.d_queue)};
     for (void **q : ptrs) {
         cudaFree(*q);
         *q = nullptr;
@@ -298,6 +302,7 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
         }
         kp.pdl_wait = (mode == 1 && c1 > c0 && !W.no_pdl) ? 1 : 0;   // fp8 launch overlaps the cast tail
         kp.timeline = mode == 0 ? W.d_timeline : nullptr;
+        kp.queue = (mode == 0 && W.variant >= kCastTmaVariant && !W.static_items) ? W.d_queue : nullptr;
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
         kp.pdl_wait = 0;
     }

@@ -71,6 +71,8 @@ def test_fill_matches_synth(rt):
     llrl, runner = rt
     for sdt in ("f32", "bf16"):
         job = _toy_job(rt, "toy", 3, 2, 4, sdt, "bf16")
+        for t in job.src.values():
+            t.zero_()                     # padding: the fill writes the pieces only (as host_src)
         job.fill(7)
         ol = oracle.Layout(job.model, 3, 2, 4, sdt, "bf16")
         want = harness.host_src(ol, 7)
