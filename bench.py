@@ -334,12 +334,14 @@ def run_llrl(args):
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(args.steps)]
             for k in range(args.steps):
-                if small:
-                    with torch.cuda.stream(stream):
-                        flush.fill_(k & 0xFF)
                 torch.cuda.synchronize()
                 _barrier()
                 with torch.cuda.stream(stream):
+                    if small:
+                        # the flush (a 512 MB write, ~0.1 ms) also keeps the GPU busy while
+                        # the host enqueues the sync, so the events time the GPU's work
+                        # only, not the host's launch path
+                        flush.fill_(k & 0xFF)
                     evs[k][0].record(stream)
                     job.sync()
                     evs[k][1].record(stream)

@@ -233,6 +233,14 @@ llrl_status llrl_mc_create(int n_devices, int64_t bytes, int *fd_out, int64_t *s
 llrl_status llrl_mc_import(int fd, int n_devices, int64_t size, llrl_mcbuf **out);
 llrl_status llrl_mc_join(llrl_mcbuf *m, int device, void **local_ptr, void **mc_ptr);
 void llrl_mc_destroy(llrl_mcbuf *m);
+/* Unicast access to a peer GPU's memory of the same multicast object (for the
+ * plan's egress split: a share of a replica position's items is pushed to every
+ * replica as plain peer stores, the rest multicast): llrl_mc_export_local gives a
+ * POSIX fd of this process's bound memory (after llrl_mc_join), llrl_mc_map_peer
+ * maps a peer's fd into this process for `device` (*ptr: that replica's rank
+ * buffer as seen here).  Unmapped by llrl_mc_destroy. */
+llrl_status llrl_mc_export_local(const llrl_mcbuf *m, int *fd_out);
+llrl_status llrl_mc_map_peer(llrl_mcbuf *m, int fd, int device, void **ptr);
 llrl_status llrl_plan_set_multicast(llrl_plan *p, int device, void *const *dst_mc_ptrs);
 
 /* ---- NVFP4 with a caller-supplied tensor amax (R16 in one pass) ----------------

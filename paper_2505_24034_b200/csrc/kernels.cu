@@ -694,7 +694,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    __shared__ int s_item[kCastStages], s_chunk[kCastStages];   // what each stage holds (-1: end of work)
+    // what each stage holds: item index (-1: end of work), the item, the chunk
+    __shared__ int s_item[kCastStages];
+    __shared__ Item s_it[kCastStages];
+    __shared__ Chunk s_ch[kCastStages];
     if (warp == 0) {
         // producer: claims items and stages the rows of every vector item; scalar
         // items pass a token.  Claims are dynamic (one atomicAdd per item on the
@@ -702,7 +705,9 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         // current item's copies): CTAs that drew cheap (local) items take more, so
         // all finish together instead of the last CTA setting the sync's tail
         // (static striding when P.queue is null).  Each stage carries its item and
-        // chunk in s_item / s_chunk, written before the arrive (release -> acquire).
+        // chunk geometry in s_item / s_it / s_ch, written before the arrive (release
+        // -> acquire), so workers and storer neither reload items nor redo the
+        // chunk arithmetic.
         int n = 0;
         unsigned claimed = 0;
         if (P.queue && lane == 0) claimed = atomicAdd(P.queue, 1u);
@@ -716,15 +721,16 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
                 mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+                const Chunk c = (it.flags & F_VEC) ? cast_chunk<SB>(it, es, rows_per, segs, k) : Chunk{0, 0, 0, 0};
                 if (lane == 0) {
                     s_item[st] = i;
-                    s_chunk[st] = k;
+                    s_it[st] = it;
+                    s_ch[st] = c;
                 }
                 if (!(it.flags & F_VEC)) {
                     if (lane == 0) mbar_arrive(&full_bar[st]);
                     continue;
                 }
-                const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                 if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
                 __syncwarp();
                 unsigned char *dst = stages + st * kStride;
@@ -751,9 +757,8 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         for (int n = 0;; n++) {
             const int st = n % kCastStages;
             mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
-            const int i = s_item[st];
-            if (i < 0) break;
-            const Item it = P.items[i];
+            if (s_item[st] < 0) break;
+            const Item it = s_it[st];
             const bool vec = it.flags & F_VEC;
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
@@ -774,9 +779,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                     continue;
                 }
                 if (lane == 0) {
-                    int rows_per, segs;
-                    cast_chunks<SB>(it, es, &rows_per, &segs);
-                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, s_chunk[st]);
+                    const Chunk c = s_ch[st];
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
                     // rows contiguous in the destination (chunk spans whole rows): one bulk store
                     const int nrow = c.nc == it.dst_ld ? 1 : c.nr, nel = c.nc == it.dst_ld ? c.nr * c.nc : c.nc;
@@ -803,13 +806,12 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         for (int n = 0;; n++) {
             const int st = n % kCastStages;
             mbar_wait(&full_bar[st], (n / kCastStages) & 1);
-            const int i = s_item[st], k = s_chunk[st];
-            if (i < 0) {                          // end of work: pass the token to the storer
+            if (s_item[st] < 0) {                 // end of work: pass the token to the storer
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
                 break;
             }
-            const Item it = P.items[i];
+            const Item it = s_it[st];
             const bool dst_f32 = it.flags & F_DST_F32;
             char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
@@ -831,8 +833,6 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
                 continue;
             }
-            int rows_per, segs;
-            cast_chunks<SB>(it, es, &rows_per, &segs);
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 unsigned char *in = stages + st * kStride;
                 unsigned char *out = in + kCastStageBytes;
                 if (cast || mx) {
-                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
+                    const Chunk c = s_ch[st];
                     if (cast) {
                         const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
                         for (int u = wt; u < nunits; u += kCastWorkers) {

@@ -84,6 +84,7 @@ struct llrl_mcbuf {
     CUmemGenericAllocationHandle mem = 0;    // local physical memory bound to the object
     CUdeviceptr local = 0, mcva = 0;         // unicast VA of the local memory, multicast VA
     bool bound = false;
+    std::vector<std::pair<CUdeviceptr, CUmemGenericAllocationHandle>> peers;   // peers' memory mapped here
 };
 
 extern "C" {
@@ -180,10 +181,50 @@ llrl_status llrl_mc_join(llrl_mcbuf *m, int device, void **local_ptr, void **mc_
     return LLRL_OK;
 }
 
+llrl_status llrl_mc_export_local(const llrl_mcbuf *m, int *fd_out) {
+    if (!m || !fd_out || !m->bound) { set_error("llrl_mc_export_local: invalid argument (join first)"); return LLRL_E_INVALID; }
+    int fd = -1;
+    CUK(drv().exportHandle(&fd, m->mem, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
+    *fd_out = fd;
+    return LLRL_OK;
+}
+
+llrl_status llrl_mc_map_peer(llrl_mcbuf *m, int fd, int device, void **ptr) {
+    if (!m || fd < 0 || device < 0 || !ptr) { set_error("llrl_mc_map_peer: invalid argument"); return LLRL_E_INVALID; }
+    Drv &d = drv();
+    if (!d.ok) { set_error("multicast driver entry points unavailable"); return LLRL_E_UNSUPPORTED; }
+    CUmemGenericAllocationHandle h = 0;
+    CUK(d.importHandle(&h, reinterpret_cast<void *>(intptr_t(fd)), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+        "cuMemImportFromShareableHandle(peer)");
+    CUdeviceptr va = 0;
+    CUresult r = d.addrReserve(&va, m->size, m->gran, 0, 0);
+    if (r == CUDA_SUCCESS) r = d.memMap(va, m->size, 0, h, 0);
+    if (r == CUDA_SUCCESS) {
+        CUmemAccessDesc ad;
+        ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ad.location.id = device;
+        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        r = d.setAccess(va, m->size, &ad, 1);
+    }
+    if (r != CUDA_SUCCESS) {
+        if (va) { d.memUnmap(va, m->size); d.addrFree(va, m->size); }
+        d.memRelease(h);
+        return cu_fail(r, "llrl_mc_map_peer");
+    }
+    m->peers.push_back({va, h});
+    *ptr = reinterpret_cast<void *>(va);
+    return LLRL_OK;
+}
+
 void llrl_mc_destroy(llrl_mcbuf *m) {
     if (!m) return;
     Drv &d = drv();
     if (d.ok) {
+        for (auto &pv : m->peers) {
+            d.memUnmap(pv.first, m->size);
+            d.addrFree(pv.first, m->size);
+            d.memRelease(pv.second);
+        }
         if (m->mcva) { d.memUnmap(m->mcva, m->size); d.addrFree(m->mcva, m->size); }
         if (m->local) { d.memUnmap(m->local, m->size); d.addrFree(m->local, m->size); }
         if (m->bound) {

@@ -71,7 +71,7 @@ struct Builder {
     static int mc_unicast_period() {
         static const int k = [] {
             const char *v = getenv("LLRL_MC_UNICAST_PERIOD");
-            return v ? std::max(0, atoi(v)) : 0;
+            return v ? std::max(0, atoi(v)) : 9;
         }();
         return k;
     }

@@ -37,7 +37,7 @@ EXPORTS = [
     "llrl_sync", "llrl_sync_host", "llrl_plan_num_groups", "llrl_plan_group_range", "llrl_plan_set_max_ctas", "llrl_sync_group", "llrl_sync_num_launches", "llrl_fill_synthetic", "llrl_mc_create", "llrl_mc_import", "llrl_mc_join",
     "llrl_mc_destroy", "llrl_plan_set_multicast", "llrl_last_error", "llrl_plan_nv_num_tensors",
     "llrl_plan_nv_tensor", "llrl_plan_nv_tensor_sources", "llrl_sync_nv_amax", "llrl_nccl_unique_id",
-    "llrl_nccl_attach", "llrl_plan_nccl_info", "llrl_debug_timeline",
+    "llrl_nccl_attach", "llrl_plan_nccl_info", "llrl_debug_timeline", "llrl_mc_export_local", "llrl_mc_map_peer",
     "llrl_version",
 ]
 
@@ -130,6 +130,8 @@ _sig("llrl_mc_create", [_int, _i64, _P(_int), _P(_i64), _P(_vp)])
 _sig("llrl_mc_import", [_int, _int, _i64, _P(_vp)])
 _sig("llrl_mc_join", [_vp, _int, _P(_vp), _P(_vp)])
 _sig("llrl_mc_destroy", [_vp], None)
+_sig("llrl_mc_export_local", [_vp, _P(_int)])
+_sig("llrl_mc_map_peer", [_vp, _int, _int, _P(_vp)])
 _sig("llrl_plan_set_multicast", [_vp, _int, _P(_vp)])
 _sig("llrl_comm_create", [_int, _P(_vp)])
 _sig("llrl_comm_export", [_vp, ctypes.c_char_p])
@@ -433,6 +435,18 @@ class McBuf:
         a, b = _vp(), _vp()
         _check(_lib.llrl_mc_join(self._h, device, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    def export_local(self):
+        """POSIX fd of this process's memory bound to the object (after join)."""
+        fd = _int()
+        _check(_lib.llrl_mc_export_local(self._h, ctypes.byref(fd)))
+        return fd.value
+
+    def map_peer(self, fd, device):
+        """Map a peer's bound memory (its exported fd) for `device` -> pointer."""
+        p = _vp()
+        _check(_lib.llrl_mc_map_peer(self._h, fd, device, ctypes.byref(p)))
+        return p.value
 
     def close(self):
         if self._h:

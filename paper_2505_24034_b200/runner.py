@@ -79,6 +79,7 @@ class SyncJob:
                     for r in range(self.S.n_ranks) if self.src_dev[r] == self.device}
         self._mc = []
         self.mc_ranks = set()
+        self._mc_peer_ptrs = {}
         self.dst = {}
         if multicast and self.world > 1:
             self._setup_multicast()
@@ -91,7 +92,8 @@ class SyncJob:
         self.comm = None
         self._opened = []
         self.src_ptrs = [self.src[r].data_ptr() if r in self.src else 0 for r in range(self.S.n_ranks)]
-        self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else 0 for g in range(self.D.n_ranks)]
+        self.dst_ptrs = [self.dst[g].data_ptr() if g in self.dst else self._mc_peer_ptrs.get(g, 0)
+                         for g in range(self.D.n_ranks)]
         # NEXT f3: double-buffered generator weights.  `dst` is what the next sync
         # writes, `front` what the generator reads; swap() exchanges them once a
         # sync completed, so generation continues during the sync.
@@ -221,6 +223,18 @@ class SyncJob:
             self.mc_ranks.update(d * ns + pos for d in range(self.cfg.dp_gen))
         self._mc = bufs
         self.plan.set_multicast(self.device, dst_mc)
+        dist.barrier()
+        # egress split (plan.cpp: a share of each position's items is pushed to every
+        # replica as plain peer stores): map the peers' replica memory here
+        peer_fds = _exchange_fds(name + "-x", self.rank, self.world, [b.export_local() for b in bufs])
+        for k, (pos, buf) in enumerate(zip(positions, bufs)):
+            for d in range(self.cfg.dp_gen):
+                q = d * ns + pos
+                if self.dst_dev[q] != self.device:
+                    self._mc_peer_ptrs[q] = buf.map_peer(peer_fds[self.dst_dev[q]][k], self.device)
+        for fds in peer_fds.values():
+            for fd in fds:
+                os.close(fd)
         dist.barrier()
 
     def swap(self):
@@ -355,6 +369,50 @@ def map_peers(all_meta, my_device, src_ptrs, dst_ptrs, opener, extra=None):
                     bases[h] = opener(h)
                 ptrs[int(r)] = bases[h] + off
     return flags
+
+
+def _exchange_fds(tag, rank, world, fds):
+    """All-to-all exchange of POSIX fds between the processes of one node (one
+    abstract Unix socket per process, SCM_RIGHTS); process rank == GPU ordinal.
+    Returns {peer rank: [its fds, in order]}; closes the fds sent."""
+    import socket
+    import threading
+    import time
+    dist = _dist()
+
+    def sock_name(r):
+        return f"\0{tag}-{r}"
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(sock_name(rank))
+    srv.listen(world)
+    dist.barrier()
+    got = {}
+
+    def acceptor():
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            msg, rfds, _, _ = socket.recv_fds(conn, 64, max(1, len(fds)))
+            got[int(msg.decode())] = list(rfds)
+            conn.close()
+    th = threading.Thread(target=acceptor, daemon=True)
+    th.start()
+    for p in range(world):
+        if p == rank:
+            continue
+        c = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        for _ in range(400):
+            try:
+                c.connect(sock_name(p))
+                break
+            except OSError:
+                time.sleep(0.05)
+        socket.send_fds(c, [str(rank).encode()], fds)
+        c.close()
+    th.join(timeout=120)
+    srv.close()
+    for fd in fds:
+        os.close(fd)
+    return got
 
 
 def spec_for(name: str, n_gpus: int) -> JobSpec:

@@ -111,6 +111,21 @@ def _worker(rank, world, port, q):
                 # the kernels write replica 0 only
                 runs = plan.runs()
                 assert runs.size and int(runs["dst_rank"].max()) < ns
+        # runner._exchange_fds (multicast egress split: every process maps its peers'
+        # replica memory): all-to-all fd passing over Unix sockets, checked with pipes
+        pipes = [os.pipe() for _ in range(2)]
+        got = runner._exchange_fds(f"llrl-test-{port}", rank, world, [w for _, w in pipes])
+        assert sorted(got) == [p for p in range(world) if p != rank] and all(len(v) == 2 for v in got.values())
+        for p, fds in got.items():
+            for k, fd in enumerate(fds):
+                os.write(fd, f"{rank}>{p}:{k};".encode())
+                os.close(fd)
+        dist.barrier()
+        for k, (r, _) in enumerate(pipes):
+            data = os.read(r, 4096).decode()
+            os.close(r)
+            want = sorted(f"{s}>{rank}:{k}" for s in range(world) if s != rank)
+            assert sorted(x for x in data.split(";") if x) == want, data
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))

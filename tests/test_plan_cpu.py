@@ -408,3 +408,23 @@ def test_plan_algorithmic_bytes_equal_layout_bytes(L, name):
     dev = [plan.device_bytes(d) for d in range(st.n_devices)]
     assert sum(b["hbm_write"] for b in dev) == st.dst_bytes and sum(b["hbm_read"] for b in dev) == st.src_bytes
     assert sum(plan.device_info(d).nv_amax_read_bytes for d in range(st.n_devices)) == want_reread
+
+
+def test_nvfp4_group_ranges_include_tensor_scales(L):
+    """a layer group's generator byte range covers its NVFP4 tensors'
+    fp32 tensor scales (placed after the scale grid), so a caller consuming one
+    group at a time gets them."""
+    m = MODELS["toy"]
+    S, D = L.describe(m, 2, 2, 4, "bf16", "nvfp4")
+    plan = L.Plan(S, D, [0] * S.n_ranks, [0] * D.n_ranks)
+    n = plan.num_groups()
+    for g in range(D.n_ranks):
+        for gp in range(D.n_params):
+            v = D.param_view(g, gp)
+            if not v.quantised:
+                continue
+            assert v.tensor_scale_off > v.scale_off
+            grp = 1 + v.layer                     # groups: embed | layers | final_norm + lm_head
+            lo, hi = plan.group_range(1, g, grp)
+            assert lo <= v.byte_off and v.tensor_scale_off + 4 <= hi, (g, gp, lo, hi)
+    assert n == m.n_layers + 2
