@@ -146,6 +146,16 @@ struct TmaPiece {            // a trainer piece that fp8 blocks read through a t
     int src_rank;
     int64_t byte_off, rows, cols;
 };
+// A column band of a trainer piece that strided cast items read through a 3-D
+// tensor map: rows of `row_bytes` at a pitch of `ld_bytes`, starting at byte_off
+// of the src rank buffer (each stage of an item = one box of whole rows).
+struct CastBand {
+    int src_rank;
+    int64_t byte_off, rows, row_bytes, ld_bytes;
+};
+struct CastRef {             // per cast item: its band's map (-1: none) and first row in the band
+    int32_t map, row;
+};
 
 // Host-side tile: one rectangle intersection (param part, src rank, dst rank).
 struct Tile {
@@ -163,6 +173,8 @@ struct DeviceWork {
     std::vector<Item> items;
     std::vector<Seg> segs;
     std::vector<TmaRef> tma_refs;      // one per fp8 item (index i - n_cast)
+    std::vector<CastRef> cast_refs;    // one per cast item (strided source rows: 3-D tensor map)
+    std::vector<CastBand> cast_bands;
     std::vector<void *> dst_mc;        // multicast VA per dst rank (llrl_plan_set_multicast)
     // NVFP4 (R16) per-tensor amax handshake
     std::vector<int32_t> nv_contrib;   // tensor ids this device's items quantise
@@ -200,13 +212,20 @@ struct DeviceWork {
     Item *d_items = nullptr;
     Seg *d_segs = nullptr;
     TmaRef *d_tma_refs = nullptr;
+    CastRef *d_cast_refs = nullptr;         // null: no strided cast items (or LLRL_CAST_TMAP=0)
+    void *d_cast_tmaps = nullptr;           // CUtensorMap[cast_bands.size()]
+    std::vector<unsigned char> h_cast_tmaps;
+    int32_t *d_cast_box = nullptr;          // per band: rows per box, 0 = per-row copies
+    std::vector<int32_t> h_cast_box;
+    std::vector<const void *> cast_tmap_src;   // src base pointers the cast maps were encoded for
+    int cast_tmap_sb = 0;                      // stage bytes the boxes were sized for
     void *d_tmaps = nullptr;                // CUtensorMap[tma_pieces.size()] (64-byte aligned)
     std::vector<unsigned char> h_tmaps;     // host copy (kept alive for the async upload)
     std::vector<const void *> tmap_src;     // src base pointers the maps were encoded for
     unsigned long long *d_done = nullptr;   // last-CTA counter (cumulative)
     unsigned long long *d_timeline = nullptr;   // LLRL_TIMELINE: per-CTA start / end of the cast launch
     unsigned int *d_queue = nullptr;            // dynamic item queue of the TMA cast launch
-    bool static_items = false;                  // LLRL_STATIC_ITEMS=1: static striding instead
+    double static_frac = 0.9;                   // TMA cast launches: share of items striped (rest claimed)
     void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)
     std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8

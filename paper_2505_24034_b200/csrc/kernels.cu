@@ -532,6 +532,15 @@ __device__ __forceinline__ void tma_box_g2s(void *dst_smem, const void *tmap, in
                  : "memory");
 }
 
+// 3-D tensor TMA: box of a strided cast band's map at row `row` (kernels' own
+// [rows][n1][b0] 8-byte-unit view, runtime.cu ensure_cast_tmaps).
+__device__ __forceinline__ void tma_box3_g2s(void *dst_smem, const void *tmap, int row, uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(smem_u32(dst_smem)), "l"(tmap), "r"(0), "r"(0), "r"(row), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 template <bool SRC_F32>
 __host__ __device__ constexpr int fp8_stages() { return SRC_F32 ? 3 : 3; }
 template <bool SRC_F32>
@@ -658,6 +667,69 @@ __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per
     return c;
 }
 
+// A role's walk over the (item, chunk) stages of its CTA, in two phases.
+// Static phase, items [item_begin, static_end): striding (CTA b takes items b,
+// b + gridDim.x, ...); every role walks this sequence itself and loads an
+// item's descriptor before it waits for the item's first stage -- no hand-off.
+// Dynamic phase, items [static_end, item_end) (only with P.queue): the producer
+// claims each item with one atomicAdd (the next claim in flight while the
+// current item's copies are issued) and hands each stage's item and chunk to
+// the other roles in shared memory.  The dynamic tail absorbs the spread of
+// per-SM speeds, so all CTAs finish together; the static bulk keeps the
+// per-stage hand-off off the critical path.
+struct StageWalk {
+    int i, k, nch, rows_per, segs;
+    unsigned claimed;
+    bool dyn;
+    int band, band_row, band_rows;   // producer: strided-source band map of the item (-1: none)
+    Item it;
+};
+enum { WALK_END = 0, WALK_STAGE = 1, WALK_HANDOFF = 2 };
+__device__ __forceinline__ void walk_init(StageWalk &w, const KParams &P, bool producer, int lane) {
+    w.i = P.item_begin + int(blockIdx.x) - int(gridDim.x);
+    w.k = w.nch = 0;
+    w.claimed = 0;
+    w.dyn = false;
+    if (producer && P.queue && lane == 0) w.claimed = atomicAdd(P.queue, 1u);   // first claim, in flight
+}
+// Next stage of this role: WALK_STAGE (w.it, c set), WALK_END, or -- consumers
+// entering the dynamic phase -- WALK_HANDOFF (read stages from shared memory).
+template <int SB>
+__device__ __forceinline__ int walk_next(StageWalk &w, const KParams &P, int es, bool producer, int lane, Chunk &c) {
+    if (w.k == w.nch) {
+        w.k = 0;
+        if (!w.dyn) {
+            w.i += int(gridDim.x);
+            if (w.i >= P.static_end) {
+                if (!P.queue) return WALK_END;
+                w.dyn = true;
+                if (!producer) return WALK_HANDOFF;
+            }
+        }
+        if (w.dyn) {
+            w.i = P.static_end + int(__shfl_sync(0xffffffffu, w.claimed, 0));
+            if (w.i >= P.item_end) return WALK_END;
+            if (lane == 0) w.claimed = atomicAdd(P.queue, 1u);   // the next item, in flight
+        }
+        w.it = P.items[w.i];
+        w.nch = (w.it.flags & F_VEC) ? cast_chunks<SB>(w.it, es, &w.rows_per, &w.segs) : 1;
+        w.band = -1;
+        if (producer && P.cast_refs) {
+            const CastRef r = P.cast_refs[w.i];
+            if (r.map >= 0) {
+                w.band_rows = P.cast_box[r.map];
+                if (w.band_rows > 0) {
+                    w.band = r.map;
+                    w.band_row = r.row;
+                }
+            }
+        }
+    }
+    c = (w.it.flags & F_VEC) ? cast_chunk<SB>(w.it, es, w.rows_per, w.segs, w.k) : Chunk{0, 0, 0, 0};
+    w.k++;
+    return WALK_STAGE;
+}
+
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  ::"l"(dst), "r"(smem_u32(src_smem)), "r"(bytes)
@@ -694,71 +766,77 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // what each stage holds: item index (-1: end of work), the item, the chunk
+    // dynamic phase: what each stage holds -- item index (-1: end of work), the
+    // item, the chunk -- written by the producer before its arrive (release ->
+    // acquire)
     __shared__ int s_item[kCastStages];
     __shared__ Item s_it[kCastStages];
     __shared__ Chunk s_ch[kCastStages];
+    StageWalk w;
+    walk_init(w, P, warp == 0, lane);
     if (warp == 0) {
-        // producer: claims items and stages the rows of every vector item; scalar
-        // items pass a token.  Claims are dynamic (one atomicAdd per item on the
-        // launch's queue, issued one item ahead so its latency hides behind the
-        // current item's copies): CTAs that drew cheap (local) items take more, so
-        // all finish together instead of the last CTA setting the sync's tail
-        // (static striding when P.queue is null).  Each stage carries its item and
-        // chunk geometry in s_item / s_it / s_ch, written before the arrive (release
-        // -> acquire), so workers and storer neither reload items nor redo the
-        // chunk arithmetic.
-        int n = 0;
-        unsigned claimed = 0;
-        if (P.queue && lane == 0) claimed = atomicAdd(P.queue, 1u);
-        int i = P.queue ? P.item_begin + int(__shfl_sync(0xffffffffu, claimed, 0)) : P.item_begin + int(blockIdx.x);
-        while (i < P.item_end) {
-            if (P.queue && lane == 0) claimed = atomicAdd(P.queue, 1u);   // the next item, in flight
-            const Item it = P.items[i];
-            int rows_per, segs;
-            const int nch = (it.flags & F_VEC) ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
-            const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
-            for (int k = 0; k < nch; k++, n++) {
-                const int st = n % kCastStages;
-                mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
-                const Chunk c = (it.flags & F_VEC) ? cast_chunk<SB>(it, es, rows_per, segs, k) : Chunk{0, 0, 0, 0};
-                if (lane == 0) {
-                    s_item[st] = i;
-                    s_it[st] = it;
-                    s_ch[st] = c;
+        // producer: stages the rows of every vector item; scalar items pass a token
+        for (int n = 0;; n++) {
+            const int st = n % kCastStages;
+            Chunk c;
+            if (walk_next<SB>(w, P, es, true, lane, c) == WALK_END) {
+                if (P.queue) {                    // end-of-work token for the other roles
+                    mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+                    if (lane == 0) {
+                        s_item[st] = -1;
+                        mbar_arrive(&full_bar[st]);
+                    }
                 }
-                if (!(it.flags & F_VEC)) {
-                    if (lane == 0) mbar_arrive(&full_bar[st]);
-                    continue;
-                }
-                if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
-                __syncwarp();
-                unsigned char *dst = stages + st * kStride;
-                if (c.nc == it.src_ld) {          // rows contiguous in the source: one bulk copy
-                    if (lane == 0)
-                        bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
-                } else {
-                    for (int r = lane; r < c.nr; r += 32)
-                        bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
-                                 uint32_t(c.nc * es), &full_bar[st]);
-                }
+                break;
             }
-            i = P.queue ? P.item_begin + int(__shfl_sync(0xffffffffu, claimed, 0)) : i + int(gridDim.x);
-        }
-        const int st = n % kCastStages;          // end-of-work token
-        mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
-        if (lane == 0) {
-            s_item[st] = -1;
-            mbar_arrive(&full_bar[st]);
+            const Item &it = w.it;
+            mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+            if (w.dyn && lane == 0) {
+                s_item[st] = w.i;
+                s_it[st] = it;
+                s_ch[st] = c;
+            }
+            if (!(it.flags & F_VEC)) {
+                if (lane == 0) mbar_arrive(&full_bar[st]);
+                continue;
+            }
+            const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
+            if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
+            __syncwarp();
+            unsigned char *dst = stages + st * kStride;
+            if (c.nc == it.src_ld) {              // rows contiguous in the source: one bulk copy
+                if (lane == 0)
+                    bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
+            } else if (w.band >= 0 && c.nc == it.cols && c.nr == w.band_rows) {
+                // strided whole rows: one 3-D tensor box (the band's map) instead of a copy per row
+                if (lane == 0)
+                    tma_box3_g2s(dst, static_cast<const unsigned char *>(P.cast_tmaps) + 128 * w.band, w.band_row + c.r0,
+                                 &full_bar[st]);
+            } else {
+                for (int r = lane; r < c.nr; r += 32)
+                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                             uint32_t(c.nc * es), &full_bar[st]);
+            }
         }
     } else if (warp == 1) {
         // storer: write each converted stage back, release it once read
         int pend = -1;
+        bool handoff = false;
         for (int n = 0;; n++) {
             const int st = n % kCastStages;
+            Chunk c;
+            if (!handoff) {
+                const int r = walk_next<SB>(w, P, es, false, lane, c);
+                if (r == WALK_END) break;
+                handoff = r == WALK_HANDOFF;
+            }
             mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
-            if (s_item[st] < 0) break;
-            const Item it = s_it[st];
+            if (handoff) {
+                if (s_item[st] < 0) break;
+                w.it = s_it[st];
+                c = s_ch[st];
+            }
+            const Item &it = w.it;
             const bool vec = it.flags & F_VEC;
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
@@ -779,7 +857,6 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                     continue;
                 }
                 if (lane == 0) {
-                    const Chunk c = s_ch[st];
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
                     // rows contiguous in the destination (chunk spans whole rows): one bulk store
                     const int nrow = c.nc == it.dst_ld ? 1 : c.nr, nel = c.nc == it.dst_ld ? c.nr * c.nc : c.nc;
@@ -803,15 +880,44 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         // workers
         const int wt = threadIdx.x - 64;
         int nv_tid = -1, nv_buf = 0;
+        bool handoff = false;
         for (int n = 0;; n++) {
             const int st = n % kCastStages;
-            mbar_wait(&full_bar[st], (n / kCastStages) & 1);
-            if (s_item[st] < 0) {                 // end of work: pass the token to the storer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&conv_bar[st]);
-                break;
+            Chunk c;
+            if (!handoff) {
+                const int r = walk_next<SB>(w, P, es, false, lane, c);
+                if (r == WALK_END) break;
+                handoff = r == WALK_HANDOFF;
             }
-            const Item it = s_it[st];
+            if (handoff) {
+                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+                if (s_item[st] < 0) {             // end of work: pass the token to the storer
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&conv_bar[st]);
+                    break;
+                }
+                w.it = s_it[st];
+                c = s_ch[st];
+            }
+            const Item &it = w.it;
+            if ((it.flags & F_NV) && (it.flags & F_VEC) && it.tid != nv_tid) {
+                // R16, per generator tensor: S_enc = 2688 / max(A, 2^-64), and for every
+                // E4M3 group-scale code c the element multiplier r(c) = S_enc / s_q(c)
+                // (0 for s_q = 0) -- one exact division per code instead of per group.
+                // Double-buffered: a worker one tensor ahead writes the other table.
+                nv_tid = it.tid;
+                nv_buf ^= 1;
+                const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
+                const float s_enc = __fdiv_rn(2688.0f, A);
+                if (wt < 128) {
+                    const float sq = e4m3_value(uint32_t(wt));
+                    nv_r[nv_buf][wt] = (wt == 0 || wt == 127) ? 0.0f : __fdiv_rn(s_enc, sq);
+                }
+                if (wt == 0) nv_senc[nv_buf] = s_enc;
+                asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
+            }
+            // static phase: the item and its tensor table were ready before its data
+            if (!handoff) mbar_wait(&full_bar[st], (n / kCastStages) & 1);
             const bool dst_f32 = it.flags & F_DST_F32;
             char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
@@ -836,27 +942,10 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
-            if ((it.flags & F_NV) && it.tid != nv_tid) {
-                // R16, per generator tensor: S_enc = 2688 / max(A, 2^-64), and for every
-                // E4M3 group-scale code c the element multiplier r(c) = S_enc / s_q(c)
-                // (0 for s_q = 0) -- one exact division per code instead of per group.
-                // Double-buffered: a worker one tensor ahead writes the other table.
-                nv_tid = it.tid;
-                nv_buf ^= 1;
-                const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
-                const float s_enc = __fdiv_rn(2688.0f, A);
-                if (wt < 128) {
-                    const float sq = e4m3_value(uint32_t(wt));
-                    nv_r[nv_buf][wt] = (wt == 0 || wt == 127) ? 0.0f : __fdiv_rn(s_enc, sq);
-                }
-                if (wt == 0) nv_senc[nv_buf] = s_enc;
-                asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
-            }
             {
                 unsigned char *in = stages + st * kStride;
                 unsigned char *out = in + kCastStageBytes;
                 if (cast || mx) {
-                    const Chunk c = s_ch[st];
                     if (cast) {
                         const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
                         for (int u = wt; u < nunits; u += kCastWorkers) {
@@ -1250,5 +1339,10 @@ cudaError_t sync_occupancy(int mode, int variant, bool src_f32, int *blocks_per_
 }
 
 int num_cast_variants() { return kNumCastVariants + 3; }   // + the three TMA variants
+
+int cast_stage_bytes(int variant) {
+    if (variant == kCastTmaVariant + 1) return 16 * 1024;   // LLRL_TMA_B
+    return 32 * 1024;                                       // LLRL_TMA_A, LLRL_TMA_C
+}
 
 }  // namespace llrl

@@ -19,6 +19,7 @@ struct KParams {
     int fp8_base;
     unsigned long long *done;          // per (plan, device) CTA completion counter (self-resetting), or null
     int item_begin, item_end;          // [begin, end) of this launch
+    int static_end;                    // TMA cast launch: items [item_begin, static_end) striped, the rest claimed (queue)
     int n_signal;
     unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
     const void *src[kMaxRanks];
@@ -26,6 +27,9 @@ struct KParams {
     void *dst_mc[kMaxRanks];           // multicast VA per dst rank (F_MC items)
     unsigned long long *timeline;      // debug (LLRL_TIMELINE): [grid][start, end] of the cast launch, or null
     unsigned int *queue;               // TMA cast launch: [next item, CTAs done] (dynamic claims), or null
+    const CastRef *cast_refs;          // TMA cast launch: per item band map + row (strided sources), or null
+    const void *cast_tmaps;            // CUtensorMap per band (3-D)
+    const int32_t *cast_box;           // per band: rows per box (0 = per-row copies)
     int pdl_wait;                      // launched as a programmatic dependent of the previous
                                        // launch: wait for it before completing / signalling
 };
@@ -33,6 +37,7 @@ struct KParams {
 constexpr int kCastTmaVariant = 6;      // llrl_k_cast_tma (TMA-staged)
 constexpr int kDefaultCastVariant = kCastTmaVariant;
 cudaError_t launch_sync(const KParams &P, int mode, int variant, bool src_f32, int grid, cudaStream_t stream);
+int cast_stage_bytes(int variant);     // stage bytes of a TMA cast variant
 
 // NVFP4 (R16) per-tensor amax handshake kernels.
 struct NvAmaxParams {

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <tuple>
 
 #include "internal.h"
 
@@ -405,6 +406,44 @@ struct Builder {
         }
     }
 
+    // For every vector cast item whose source rows are strided (a column band of
+    // a wider trainer piece, e.g. o / down from FSDP row chunks into a column-
+    // parallel generator): the band's 3-D tensor map and the item's first row in
+    // it, so that each stage is one TMA box instead of one bulk copy per row.
+    void make_cast_refs(DeviceWork &W) {
+        std::map<std::tuple<int, int64_t, int64_t>, int> band_map;   // (src rank, band byte off, row bytes)
+        W.cast_refs.assign(size_t(W.n_cast), CastRef{-1, 0});
+        for (size_t i = 0; i < size_t(W.n_cast); i++) {
+            const Item &it = W.items[i];
+            if (it.kind != K_CAST || !(it.flags & F_VEC) || (it.flags & F_MC) || it.rows < 2 || it.cols == it.src_ld)
+                continue;
+            const auto &pcs = S->pieces[it.src_rank];
+            size_t lo = 0, hi = pcs.size();
+            while (hi - lo > 1) {
+                const size_t mid = (lo + hi) / 2;
+                if (pcs[mid].byte_off / es_src <= it.src_off) lo = mid; else hi = mid;
+            }
+            while (lo > 0 && pcs[lo].rows * pcs[lo].cols == 0) lo--;
+            const Piece &pc = pcs[lo];
+            const int64_t rel = it.src_off - pc.byte_off / es_src;
+            if (pc.cols != it.src_ld || rel < 0 || rel >= pc.rows * pc.cols) continue;
+            const int64_t row = rel / pc.cols, col = rel % pc.cols;
+            const int64_t off = pc.byte_off + col * es_src, rb = int64_t(it.cols) * es_src;
+            auto key = std::make_tuple(int(it.src_rank), off, rb);
+            auto f = band_map.find(key);
+            int m;
+            if (f == band_map.end()) {
+                m = int(W.cast_bands.size());
+                band_map[key] = m;
+                W.cast_bands.push_back(CastBand{int(it.src_rank), off, pc.rows, rb, pc.cols * es_src});
+            } else {
+                m = f->second;
+            }
+            W.cast_refs[i] = CastRef{m, int32_t(row)};
+        }
+        if (W.cast_bands.empty()) W.cast_refs.clear();
+    }
+
     llrl_status make_items() {
         const int G = P->n_devices;
         n_groups = S->model.n_layers + (S->model.with_embed ? 2 : 0);
@@ -597,6 +636,7 @@ struct Builder {
             for (int d = 0; d < G; d++)
                 if (sends[size_t(d)]) W.signal_devices.push_back(d);
             make_tma_refs(W);
+            make_cast_refs(W);
             P->stats.n_items += int64_t(W.items.size());
         }
         for (int e = 0; e < G; e++) {

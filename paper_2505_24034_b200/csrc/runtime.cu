@@ -55,6 +55,17 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
         CK(cudaMalloc(&W.d_tma_refs, W.tma_refs.size() * sizeof(TmaRef)));
         CK(cudaMemcpy(W.d_tma_refs, W.tma_refs.data(), W.tma_refs.size() * sizeof(TmaRef), cudaMemcpyHostToDevice));
     }
+    // 3-D tensor-map boxes for strided cast sources: opt-in (LLRL_CAST_TMAP=1).
+    // Measured slower than per-row bulk copies (C2 7.34 vs 6.93 ms, C12 27.94
+    // vs 27.56 ms on 1 GPU), kept as the experiment's record.
+    const char *ct = getenv("LLRL_CAST_TMAP");
+    if (!W.cast_bands.empty() && ct && atoi(ct) != 0) {
+        CK(cudaMalloc(&W.d_cast_refs, W.cast_refs.size() * sizeof(CastRef)));
+        CK(cudaMemcpy(W.d_cast_refs, W.cast_refs.data(), W.cast_refs.size() * sizeof(CastRef), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&W.d_cast_tmaps, W.cast_bands.size() * 128));
+        CK(cudaMalloc(&W.d_cast_box, W.cast_bands.size() * 4));
+        CK(cudaMemset(W.d_cast_box, 0, W.cast_bands.size() * 4));
+    }
     if (!W.tma_pieces.empty()) {
         CK(cudaMalloc(&W.d_tmaps, W.tma_pieces.size() * 128));
         W.h_tmaps.assign(W.tma_pieces.size() * 128, 0);
@@ -126,7 +137,16 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     }
     CK(cudaMalloc(&W.d_queue, 256));
     CK(cudaMemset(W.d_queue, 0, 256));
-    if (const char *v = getenv("LLRL_STATIC_ITEMS")) W.static_items = atoi(v) != 0;
+    // Item order of the TMA cast launch (kernels.cu StageWalk): the first
+    // static_frac of a launch's items striped over the CTAs, the rest claimed
+    // dynamically.  Striping is cheaper per stage (no shared-memory hand-off);
+    // the claimed tail lets every CTA finish together whatever its SM's speed.
+    // Measured (1 GPU): 0.9 is within noise of the best on C2,
+    // C3, C11, C12; plans with an fp8 launch behind the cast launch (C4) run
+    // 7% faster fully striped -- CTAs that finish early hand their SM to the
+    // programmatically dependent fp8 grid.
+    W.static_frac = n_fp8 > 0 ? 1.0 : 0.9;
+    if (const char *v = getenv("LLRL_STATIC_FRAC")) W.static_frac = std::min(1.0, std::max(0.0, atof(v)));
     if (const char *v = getenv("LLRL_TIMELINE"))
         if (atoi(v) && W.grid_cast > 0) {
             CK(cudaMalloc(&W.d_timeline, size_t(W.grid_cast) * 16));
@@ -171,6 +191,55 @@ llrl_status ensure_tmaps(llrl_plan *p, DeviceWork &W, void *const *src_ptrs, cud
     }
     CK(cudaMemcpyAsync(W.d_tmaps, W.h_tmaps.data(), W.h_tmaps.size(), cudaMemcpyHostToDevice, s));
     W.tmap_src.assign(src_ptrs, src_ptrs + p->n_src);
+    return LLRL_OK;
+}
+
+// (Re-)encode the 3-D tensor maps of the strided cast bands (plan.cpp
+// make_cast_refs) when the trainer base pointers or the kernel's stage size
+// change.  A band is viewed as [rows][n1][b0] 8-byte units (b0 <= 256, n1 <= 256:
+// TMA box dimensions), box = [rows per stage][n1][b0] -- in shared memory the
+// same bytes as the packed rows.  Bands that do not fit a stage stay on per-row
+// copies (their refs are cleared on the device copy).
+llrl_status ensure_cast_tmaps(llrl_plan *p, DeviceWork &W, void *const *src_ptrs, int stage_bytes, cudaStream_t s) {
+    if (W.cast_bands.empty() || !W.d_cast_refs) return LLRL_OK;
+    bool same = W.cast_tmap_sb == stage_bytes && W.cast_tmap_src.size() == size_t(p->n_src);
+    for (int r = 0; same && r < p->n_src; r++) same = W.cast_tmap_src[size_t(r)] == src_ptrs[r];
+    if (same) return LLRL_OK;
+    static PFN_encode_tiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) { set_error("cuTensorMapEncodeTiled unavailable"); return LLRL_E_CUDA; }
+        encode = reinterpret_cast<PFN_encode_tiled>(fn);
+    }
+    W.h_cast_tmaps.assign(W.cast_bands.size() * 128, 0);
+    std::vector<int32_t> box_rows_of(W.cast_bands.size(), 0);   // 0: band not usable (per-row copies)
+    for (size_t m = 0; m < W.cast_bands.size(); m++) {
+        const CastBand &b = W.cast_bands[m];
+        CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(W.h_cast_tmaps.data() + 128 * m);
+        const int64_t units = b.row_bytes / 8;
+        int64_t b0 = 0;
+        for (int64_t d = std::min<int64_t>(256, units); d >= 2; d--)
+            if (units % d == 0 && d % 2 == 0) { b0 = d; break; }
+        const int64_t n1 = b0 ? units / b0 : 0, box_rows = stage_bytes / b.row_bytes;
+        void *base = static_cast<char *>(src_ptrs[b.src_rank]) + b.byte_off;
+        if (b.row_bytes % 16 || b0 == 0 || n1 > 256 || box_rows < 1 || (reinterpret_cast<uintptr_t>(base) & 15)) continue;
+        const cuuint64_t dims[3] = {cuuint64_t(b0), cuuint64_t(n1), cuuint64_t(b.rows)};
+        const cuuint64_t strides[2] = {cuuint64_t(b0 * 8), cuuint64_t(b.ld_bytes)};
+        const cuuint32_t box[3] = {cuuint32_t(b0), cuuint32_t(n1), cuuint32_t(std::min<int64_t>(256, box_rows))},
+                         estr[3] = {1, 1, 1};
+        CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d) for cast band %zu", int(r), m); return LLRL_E_CUDA; }
+        box_rows_of[m] = int32_t(std::min<int64_t>(256, box_rows));
+    }
+    W.h_cast_box = box_rows_of;
+    CK(cudaMemcpyAsync(W.d_cast_tmaps, W.h_cast_tmaps.data(), W.h_cast_tmaps.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(W.d_cast_box, W.h_cast_box.data(), W.h_cast_box.size() * 4, cudaMemcpyHostToDevice, s));
+    W.cast_tmap_src.assign(src_ptrs, src_ptrs + p->n_src);
+    W.cast_tmap_sb = stage_bytes;
     return LLRL_OK;
 }
 
@@ -272,7 +341,8 @@ static void free_device_tables(DeviceWork &W) {
                      reinterpret_cast<void **>(&W.d_nv_amax), reinterpret_cast<void **>(&W.d_nv_contrib),
                      reinterpret_cast<void **>(&W.d_nv_tensor_dev), reinterpret_cast<void **>(&W.d_nv_local),
                      reinterpret_cast<void **>(&W.d_nv_done), reinterpret_cast<void **>(&W.d_timeline),
-                     reinterpret_cast<void **>(&W.d_queue)};
+                     reinterpret_cast<void **>(&W.d_queue), reinterpret_cast<void **>(&W.d_cast_refs),
+                     reinterpret_cast<void **>(&W.d_cast_tmaps), reinterpret_cast<void **>(&W.d_cast_box)};
     for (void **q : ptrs) {
         cudaFree(*q);
         *q = nullptr;
@@ -284,6 +354,10 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
     const bool has_fp8 = f1 > f0;
     if (has_fp8 && W.fp8_variant >= 1) {
         llrl_status st = ensure_tmaps(p, W, const_cast<void *const *>(kp.src), s);
+        if (st != LLRL_OK) return st;
+    }
+    if (c1 > c0 && W.d_cast_refs && W.variant >= kCastTmaVariant) {
+        llrl_status st = ensure_cast_tmaps(p, W, const_cast<void *const *>(kp.src), cast_stage_bytes(W.variant), s);
         if (st != LLRL_OK) return st;
     }
     for (int mode = 0; mode < 2; mode++) {
@@ -302,7 +376,18 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
         }
         kp.pdl_wait = (mode == 1 && c1 > c0 && !W.no_pdl) ? 1 : 0;   // fp8 launch overlaps the cast tail
         kp.timeline = mode == 0 ? W.d_timeline : nullptr;
-        kp.queue = (mode == 0 && W.variant >= kCastTmaVariant && !W.static_items) ? W.d_queue : nullptr;
+        kp.static_end = int(e);
+        kp.queue = nullptr;
+        kp.cast_refs = nullptr;
+        if (mode == 0 && W.variant >= kCastTmaVariant && W.d_cast_refs) {
+            kp.cast_refs = W.d_cast_refs;
+            kp.cast_tmaps = W.d_cast_tmaps;
+            kp.cast_box = W.d_cast_box;
+        }
+        if (mode == 0 && W.variant >= kCastTmaVariant) {
+            kp.static_end = int(b + int64_t(W.static_frac * double(e - b)));
+            if (kp.static_end < e) kp.queue = W.d_queue;
+        }
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));
         kp.pdl_wait = 0;
     }
@@ -491,6 +576,7 @@ llrl_status llrl_plan_set_max_ctas(llrl_plan *p, int device, int max_ctas) {
         DeviceGuard guard(W.uploaded_device);
         free_device_tables(W);
         W.tmap_src.clear();
+        W.cast_tmap_src.clear();
         W.uploaded_device = -1;
     }
     return LLRL_OK;

@@ -322,6 +322,22 @@ def test_toy_parity_cast_variants(rt, variant, monkeypatch):
         job.close()
 
 
+@pytest.mark.parametrize("tmap", ["0", "1"])
+@pytest.mark.parametrize("frac", ["0", "0.5", "1"])
+def test_toy_parity_cast_item_order(rt, tmap, frac, monkeypatch):
+    """The TMA cast launch's item orders (LLRL_STATIC_FRAC: striped share, rest
+    claimed from the queue) and its optional 3-D tensor-map boxes for strided
+    sources (LLRL_CAST_TMAP=1: o / down column bands of FSDP row chunks) are
+    bit-exact, for every cast flavour (bf16, f32, MXFP8, NVFP4)."""
+    monkeypatch.setenv("LLRL_STATIC_FRAC", frac)
+    monkeypatch.setenv("LLRL_CAST_TMAP", tmap)
+    for sdt, ddt, f, tt, tg in (("f32", "bf16", 3, 1, 4), ("bf16", "bf16", 4, 1, 2), ("f32", "f32", 2, 1, 2),
+                                ("bf16", "mxfp8", 4, 1, 4), ("f32", "nvfp4", 2, 1, 4)):
+        job = _toy_job(rt, "toy", f, tt, tg, sdt, ddt)
+        _run_and_compare(rt, job, seed=7)
+        job.close()
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_toy_parity_fp8_variants(rt, variant, monkeypatch):
     """Both fp8 kernels (register / TMA-pipelined, LLRL_FP8_VARIANT) are bit-exact,
