@@ -354,6 +354,23 @@ def run_llrl(args):
                     job.sync()
                     ev[k + 1].record(stream)
         _barrier()
+    floor_us = None
+    if small:
+        # context for the isolated-sync number: the same protocol (flush, event,
+        # one kernel, event) around a one-byte torch kernel -- the launch + event
+        # floor any single-kernel sync pays on this box
+        fl = []
+        for k in range(args.steps):
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                flush[:1].add_(1)
+                b.record(stream)
+            fl.append((a, b))
+        torch.cuda.synchronize()
+        floor_us = round(1000 * sorted(a.elapsed_time(b) for a, b in fl)[len(fl) // 2], 2)
     if args.step_sync or small:
         step_ms = [_allmax(a.elapsed_time(b)) for a, b in evs]
         ms = sum(step_ms) / len(step_ms)
@@ -411,6 +428,11 @@ def run_llrl(args):
         e2e = _e2e(job, args)
 
     comp = _nccl_comparator(job, args) if (args.comparator and args.gpus > 1) else None
+    if args.comparator and args.gpus > 1:
+        if cfg.src_dtype == cfg.dst_dtype:                 # copy engines cannot cast
+            comp.update(_ce_comparator(job, args))
+        if cfg.fsdp > 1:
+            comp.update(_allgather_comparator(job, args))
     ovl = _overlap(job, args) if args.overlap else None
 
     tot = job.plan.stats()
@@ -431,6 +453,7 @@ def run_llrl(args):
                            "nvlink_GBps_per_gpu_max": round(nvl_per_gpu, 1)},
             "roofline": roof,
             "gpu_launches": launches,
+            **({"event_floor_us": floor_us} if floor_us is not None else {}),
             "clocks": clk.summary(),
         }
         if e2e:
@@ -684,6 +707,159 @@ def _nccl_comparator(job, args):
         return res
     del inp, out
     return res
+
+
+def _rectangles(runs):
+    """Coalesce the plan's canonical 1-D runs (llrl_plan_get_runs, emission order)
+    into 2-D copies: maximal sequences of runs of one (param, src rank, dst rank,
+    len) whose src and dst offsets advance by constant strides.  Returns arrays
+    (src_rank, dst_rank, src_off, dst_off, len, rows, src_step, dst_step) in
+    elements; a 1-row rectangle has steps = len."""
+    import numpy as np
+    n = len(runs)
+    if n == 0:
+        return [np.zeros(0, np.int64)] * 8
+    # one key's runs side by side (the plan interleaves src ranks row by row),
+    # emission order kept within a key
+    runs = runs[np.lexsort((np.arange(n), runs["len"], runs["dst_rank"], runs["src_rank"], runs["src_param"]))]
+    so, do, ln = runs["src_off"], runs["dst_off"], runs["len"]
+    key = np.ones(n, bool)                 # key[i]: run i differs in key from run i-1
+    key[1:] = ((runs["src_param"][1:] != runs["src_param"][:-1]) | (runs["src_rank"][1:] != runs["src_rank"][:-1])
+               | (runs["dst_rank"][1:] != runs["dst_rank"][:-1]) | (ln[1:] != ln[:-1]))
+    ds = np.zeros(n, np.int64)
+    dd = np.zeros(n, np.int64)
+    ds[1:] = so[1:] - so[:-1]
+    dd[1:] = do[1:] - do[:-1]
+    chg = np.zeros(n, bool)                # delta into run i differs from the delta into run i-1
+    chg[2:] = (ds[2:] != ds[1:-1]) | (dd[2:] != dd[1:-1])
+    starts = []
+    prev_start = -2
+    # run i opens a rectangle if its key changes, or its delta breaks the current
+    # rectangle's stride (the stride is set by a rectangle's second run: i - 1
+    # being a start means run i is that second run, whatever its delta)
+    for i in np.nonzero(key | chg)[0].tolist():
+        if key[i] or (i - 1 != prev_start):
+            starts.append(i)
+            prev_start = i
+    st = np.array(starts, np.int64)
+    en = np.append(st[1:], n)
+    rows = en - st
+    s_step = np.where(rows > 1, ds[np.minimum(st + 1, n - 1)], ln[st])
+    d_step = np.where(rows > 1, dd[np.minimum(st + 1, n - 1)], ln[st])
+    return (runs["src_rank"][st].astype(np.int64), runs["dst_rank"][st].astype(np.int64), so[st], do[st], ln[st],
+            rows, s_step, d_step)
+
+
+def _ce_comparator(job, args):
+    """Copy-engine baseline on the real tiles (bf16 -> bf16, no cast): every
+    rectangle this GPU sources as one cudaMemcpy2DAsync from its trainer buffer
+    into the (local or IPC-mapped peer) generator buffer -- what a DMA-engine
+    transfer of the same re-layout costs, without any SM work.  The copies are
+    captured once in a CUDA graph (thousands of host calls would otherwise bind)
+    and the graph replayed per step."""
+    import numpy as np
+    import torch
+    from cuda.bindings import runtime as cr
+    cfg = job.cfg
+    es = {"bf16": 2, "f32": 4}[cfg.src_dtype]
+    sr, dr, so, do, ln, rows, ss, dstep = _rectangles(job.plan.runs())
+    mine = np.array([job.src_dev[int(r)] == job.device for r in sr], bool) if len(sr) else np.zeros(0, bool)
+    idx = np.nonzero(mine)[0]
+    bad = set(idx[(ss[idx] < ln[idx]) | (dstep[idx] < ln[idx])].tolist())   # not a forward 2-D pattern: row by row
+    s = torch.cuda.Stream(device=job.device)
+    g = torch.cuda.CUDAGraph()
+    ncopies = 0
+    with torch.cuda.stream(s):
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            h = s.cuda_stream
+            for k in idx.tolist():
+                sp, dp = job.src_ptrs[int(sr[k])], job.dst_ptrs[int(dr[k])]
+                w = int(ln[k]) * es
+                if k in bad:
+                    for j in range(int(rows[k])):
+                        cr.cudaMemcpyAsync(dp + (int(do[k]) + j * int(dstep[k])) * es,
+                                           sp + (int(so[k]) + j * int(ss[k])) * es, w,
+                                           cr.cudaMemcpyKind.cudaMemcpyDeviceToDevice, h)
+                        ncopies += 1
+                    continue
+                err = cr.cudaMemcpy2DAsync(dp + int(do[k]) * es, int(dstep[k]) * es, sp + int(so[k]) * es,
+                                           int(ss[k]) * es, w, int(rows[k]),
+                                           cr.cudaMemcpyKind.cudaMemcpyDeviceToDevice, h)[0]
+                if err != cr.cudaError_t.cudaSuccess:
+                    raise RuntimeError(f"cudaMemcpy2DAsync: {err}")
+                ncopies += 1
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    _barrier()
+    steps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(steps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    _barrier()
+    ms = _allmax(e0.elapsed_time(e1) / steps)
+    del g
+    return {"ce_memcpy2d_ms": round(ms, 3), "ce_copies_per_gpu_max": int(_allmax(float(ncopies))),
+            "ce_what": "cudaMemcpy2DAsync per rectangle of the plan's runs sourced on each GPU (copy engines, "
+                       "peer writes through the IPC mappings), captured in a CUDA graph; no cast, no SM work"}
+
+
+def _allgather_comparator(job, args):
+    """The naive alternative the plan replaces (SURVEY §8(d) "work avoided"):
+    every GPU all-gathers each layer group's full trainer bytes (NCCL
+    all_gather_into_tensor, per group: memory-bounded), then slices its own
+    generator shards out of the gathered copy.  The slice is timed as a plain
+    copy of this GPU's generator bytes of the group (byte volume only, no index
+    arithmetic), so the result is a lower bound on that baseline."""
+    import torch
+    import torch.distributed as dist
+    p = job.plan
+    ng = p.num_groups()
+    dev = torch.device("cuda", job.device)
+    src_local = [r for r in range(job.S.n_ranks) if job.src_dev[r] == job.device]
+    dst_local = [g for g in job.dst if job.dst_dev[g] == job.device]
+    chunk = []
+    for grp in range(ng):
+        mine = sum(max(0, hi - lo) for lo, hi in (p.group_range(0, r, grp) for r in src_local))
+        chunk.append(int(_allmax(float(mine))))
+    big = max(chunk) if chunk else 0
+    send = torch.empty(max(1, big), dtype=torch.uint8, device=dev)
+    gath = torch.empty(max(1, big * args.gpus), dtype=torch.uint8, device=dev)
+    dst_ranges = [[(g, *p.group_range(1, g, grp)) for g in dst_local] for grp in range(ng)]
+
+    def naive():
+        for grp in range(ng):
+            c = chunk[grp]
+            if c:
+                dist.all_gather_into_tensor(gath[:c * args.gpus], send[:c])
+            for g, lo, hi in dst_ranges[grp]:
+                if hi > lo:
+                    job.dst[g][lo:hi].copy_(gath[:hi - lo])
+
+    for _ in range(2):
+        naive()
+    torch.cuda.synchronize()
+    _barrier()
+    steps = max(3, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        naive()
+    e1.record()
+    torch.cuda.synchronize()
+    _barrier()
+    ms = _allmax(e0.elapsed_time(e1) / steps)
+    del send, gath
+    torch.cuda.empty_cache()
+    return {"naive_allgather_slice_ms": round(ms, 3), "naive_groups": ng,
+            "naive_what": "per layer group: NCCL all_gather_into_tensor of every GPU's trainer bytes of the group "
+                          "(padded to the largest), then a copy of this GPU's generator bytes of the group out of "
+                          "the gathered buffer (byte volume only: a lower bound on all-gather + slice)"}
 
 
 def _ncu_traffic(config, n):

@@ -669,7 +669,11 @@ __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per
 
 // A role's walk over the (item, chunk) stages of its CTA, in two phases.
 // Static phase, items [item_begin, static_end): striding (CTA b takes items b,
-// b + gridDim.x, ...); every role walks this sequence itself and loads an
+// b + gridDim.x, ...) or, with P.static_block, a contiguous block of them per
+// CTA (the plan interleaves destinations in proportion to their bytes, so a
+// block carries every destination's share while a stride can alias with the
+// interleave period: 4 destinations and 148 CTAs give each CTA one
+// destination); every role walks this sequence itself and loads an
 // item's descriptor before it waits for the item's first stage -- no hand-off.
 // Dynamic phase, items [static_end, item_end) (only with P.queue): the producer
 // claims each item with one atomicAdd (the next claim in flight while the
@@ -679,6 +683,7 @@ __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per
 // per-stage hand-off off the critical path.
 struct StageWalk {
     int i, k, nch, rows_per, segs;
+    int step, static_hi;             // static phase: i += step while i < static_hi
     unsigned claimed;
     bool dyn;
     int band, band_row, band_rows;   // producer: strided-source band map of the item (-1: none)
@@ -686,7 +691,16 @@ struct StageWalk {
 };
 enum { WALK_END = 0, WALK_STAGE = 1, WALK_HANDOFF = 2 };
 __device__ __forceinline__ void walk_init(StageWalk &w, const KParams &P, bool producer, int lane) {
-    w.i = P.item_begin + int(blockIdx.x) - int(gridDim.x);
+    if (P.static_block) {
+        const int64_t n = P.static_end - P.item_begin;
+        w.step = 1;
+        w.i = P.item_begin + int(n * blockIdx.x / gridDim.x) - 1;
+        w.static_hi = P.item_begin + int(n * (blockIdx.x + 1) / gridDim.x);
+    } else {
+        w.step = int(gridDim.x);
+        w.i = P.item_begin + int(blockIdx.x) - int(gridDim.x);
+        w.static_hi = P.static_end;
+    }
     w.k = w.nch = 0;
     w.claimed = 0;
     w.dyn = false;
@@ -699,8 +713,8 @@ __device__ __forceinline__ int walk_next(StageWalk &w, const KParams &P, int es,
     if (w.k == w.nch) {
         w.k = 0;
         if (!w.dyn) {
-            w.i += int(gridDim.x);
-            if (w.i >= P.static_end) {
+            w.i += w.step;
+            if (w.i >= w.static_hi) {
                 if (!P.queue) return WALK_END;
                 w.dyn = true;
                 if (!producer) return WALK_HANDOFF;

@@ -20,6 +20,7 @@ struct KParams {
     unsigned long long *done;          // per (plan, device) CTA completion counter (self-resetting), or null
     int item_begin, item_end;          // [begin, end) of this launch
     int static_end;                    // TMA cast launch: items [item_begin, static_end) striped, the rest claimed (queue)
+    int static_block;                  // static items as one contiguous block per CTA instead of a stride
     int n_signal;
     unsigned long long *signal[kMaxDevices];   // arrival counters of destination devices
     const void *src[kMaxRanks];

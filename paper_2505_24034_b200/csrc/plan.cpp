@@ -57,22 +57,27 @@ struct Builder {
     }
     std::vector<std::vector<std::vector<int>>> mc_extra;   // [exec dev][group] -> replica devices to signal
     uint64_t mc_counter = 0;
-    // elements per cast item: chunk_elems(), or 4 Ki for tiny syncs (< 64 MB of
-    // cast source in the plan: latency-bound, so more CTAs each with one short
-    // dependent round trip beat fewer longer ones)
+    // elements per cast item: chunk_elems(), or 8 Ki for tiny syncs (< 64 MB of
+    // cast source in the plan: latency-bound, so every CTA of the register kernel
+    // takes at most one item -- one dependent round trip, all its loads in
+    // flight at once; C1: 11.2 us per isolated sync vs 12.0 at 4 Ki and 12.9 at
+    // 1 Ki, profiles/r02/ab/c1_chunk.txt)
     int64_t chunk = chunk_elems();
     void size_chunks() {
         if (getenv("LLRL_CHUNK_ELEMS")) return;
         int64_t bytes = 0;
         for (const Tile &t : P->tiles) bytes += t.rows * t.cols * es_src;
-        if (bytes < (int64_t(64) << 20)) chunk = 4096;
+        if (bytes < (int64_t(64) << 20)) chunk = 8192;
     }
     // multicast egress split: every k-th multicast item is pushed to each replica
-    // instead (0 = all multicast); LLRL_MC_UNICAST_PERIOD overrides (tuning knob)
+    // instead (0 = all multicast, the default); LLRL_MC_UNICAST_PERIOD=k opts in.
+    // Measured on C9 at 4 GPUs (profiles/r02/survey4.txt): k = 0 28.2 ms, 9 29.9,
+    // 5 33.2, 3 39.3 -- the NVLS stores already occupy the egress links, so the
+    // unicast share adds time instead of filling headroom.
     static int mc_unicast_period() {
         static const int k = [] {
             const char *v = getenv("LLRL_MC_UNICAST_PERIOD");
-            return v ? std::max(0, atoi(v)) : 9;
+            return v ? std::max(0, atoi(v)) : 0;
         }();
         return k;
     }

@@ -141,12 +141,20 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     // static_frac of a launch's items striped over the CTAs, the rest claimed
     // dynamically.  Striping is cheaper per stage (no shared-memory hand-off);
     // the claimed tail lets every CTA finish together whatever its SM's speed.
-    // Measured (1 GPU): 0.9 is within noise of the best on C2,
-    // C3, C11, C12; plans with an fp8 launch behind the cast launch (C4) run
-    // 7% faster fully striped -- CTAs that finish early hand their SM to the
-    // programmatically dependent fp8 grid.
-    W.static_frac = n_fp8 > 0 ? 1.0 : 0.9;
+    // Measured (profiles/r02/ab/): with pushes to peer GPUs,
+    // all claimed (C3 13.13 vs 13.88 ms at 0.9 striped, C8 29.24 vs 30.66, C2
+    // 11.20 vs 11.43 at 4 GPUs: a CTA's share of each link follows the plan's
+    // interleave, whatever the per-link speeds); local-only syncs: 0.9 is
+    // within noise of the best on C2, C3, C11, C12 at 1 GPU, and plans with an
+    // fp8 launch behind the cast launch (C4) run 7% faster fully striped --
+    // CTAs that finish early hand their SM to the programmatically dependent
+    // fp8 grid.
+    bool pushes_remote = false;
+    for (int64_t i = 0; i < n_cast && !pushes_remote; i++)
+        pushes_remote = p->dst_device[size_t(W.items[size_t(i)].dst_rank)] != device;
+    W.static_frac = pushes_remote ? 0.0 : n_fp8 > 0 ? 1.0 : 0.9;
     if (const char *v = getenv("LLRL_STATIC_FRAC")) W.static_frac = std::min(1.0, std::max(0.0, atof(v)));
+    if (const char *v = getenv("LLRL_STATIC_BLOCK")) W.static_block = atoi(v) != 0;
     if (const char *v = getenv("LLRL_TIMELINE"))
         if (atoi(v) && W.grid_cast > 0) {
             CK(cudaMalloc(&W.d_timeline, size_t(W.grid_cast) * 16));
@@ -377,6 +385,7 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
         kp.pdl_wait = (mode == 1 && c1 > c0 && !W.no_pdl) ? 1 : 0;   // fp8 launch overlaps the cast tail
         kp.timeline = mode == 0 ? W.d_timeline : nullptr;
         kp.static_end = int(e);
+        kp.static_block = 0;
         kp.queue = nullptr;
         kp.cast_refs = nullptr;
         if (mode == 0 && W.variant >= kCastTmaVariant && W.d_cast_refs) {
@@ -386,6 +395,7 @@ static llrl_status launch_ranges(llrl_plan *p, DeviceWork &W, llrl_comm *comm, K
         }
         if (mode == 0 && W.variant >= kCastTmaVariant) {
             kp.static_end = int(b + int64_t(W.static_frac * double(e - b)));
+            kp.static_block = W.static_block;
             if (kp.static_end < e) kp.queue = W.d_queue;
         }
         CK(launch_sync(kp, mode, mode == 0 ? W.variant : W.fp8_variant, p->src_dtype == LLRL_F32, grid, s));

@@ -204,7 +204,7 @@ class Layout:
         return v
 
     def close(self):
-        if self._h:
+        if self._h and _lib is not None:     # (at interpreter exit the module may be torn down first)
             _lib.llrl_layout_destroy(self._h)
             self._h = None
 
@@ -360,7 +360,7 @@ class Plan:
                                    _ptrs(host_dst), _ptrs(src_ptrs), _ptrs(dst_ptrs), _vp(stream)))
 
     def close(self):
-        if self._h:
+        if self._h and _lib is not None:
             _lib.llrl_plan_destroy(self._h)
             self._h = None
 

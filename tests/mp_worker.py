@@ -303,6 +303,18 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2505_24034_b200 import runner
+    if "--mc-only" in sys.argv:
+        # NVLS multicast fan-out alone (run with LLRL_MC_UNICAST_PERIOD set: the
+        # opt-in unicast egress split, fixed per process)
+        toy_case(runner, world, world, 1, 1, "f32", "bf16", "colocated", dp=world, multicast=True)
+        toy_case(runner, world, 3, 1, 2, "bf16", "bf16", "colocated", dp=world // 2 if world >= 4 else 2,
+                 multicast=True)
+        toy_case(runner, world, 2, 1, 1, "bf16", "bf16", "colocated", dp=world, multicast=True)
+        dist.barrier()
+        if dist.get_rank() == 0:
+            print("MP_OK", flush=True)
+        dist.destroy_process_group()
+        return
     cases = [
         (2, 1, 2, "f32", "bf16", "disjoint"),
         (4, 1, 4, "f32", "bf16", "disjoint"),

@@ -67,3 +67,42 @@ def test_cpu_baseline_times_the_whole_workload():
     out = bench.cpu_baseline(CONFIGS["c1"], 1)
     assert out["cores"] == os.cpu_count() and out["value"] > 0 and out["single_thread_ms"] > 0
     assert out["nproc"] == os.cpu_count() and out["cpu_model"]
+
+
+def _expand(R):
+    """rectangles back to sorted (src_rank, dst_rank, src_off, dst_off, len) runs"""
+    import numpy as np
+    sr, dr, so, do, ln, rows, ss, ds = R
+    k = np.repeat(np.arange(len(sr)), rows)
+    j = np.arange(len(k)) - np.repeat(np.cumsum(rows) - rows, rows)
+    out = np.stack([sr[k], dr[k], so[k] + j * ss[k], do[k] + j * ds[k], ln[k]], 1)
+    return out[np.lexsort(out.T[::-1])]
+
+
+def test_ce_comparator_rectangles_cover_the_runs():
+    """bench.py's copy-engine comparator copies exactly the plan's runs: its 2-D
+    rectangles expand back to the runs (toy sweep and C5 at 4 GPUs), and the
+    strided o / down tiles coalesce (far fewer copies than runs)."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2505_24034_b200 import llrl, runner
+    from synth.configs import placement
+    for name, n in (("c1", 1), ("c3", 4), ("c5", 4), ("c8", 4)):
+        spec = runner.spec_for(name, n)
+        cfg = spec.cfg
+        if name != "c1":
+            spec = runner.JobSpec(cfg, n, n_layers=2)
+        S, D = llrl.describe(spec.model(), cfg.fsdp, cfg.tp_train, cfg.tp_gen, cfg.src_dtype, cfg.dst_dtype,
+                             cfg.fsdp_inner, cfg.dp_gen, cfg.pp_train, cfg.pp_gen)
+        sd, dd = placement(cfg, n)
+        P = llrl.Plan(S, D, sd, dd)
+        runs = P.runs()
+        R = bench._rectangles(runs)
+        want = np.stack([runs["src_rank"], runs["dst_rank"], runs["src_off"], runs["dst_off"], runs["len"]], 1)
+        want = want[np.lexsort(want.T[::-1])]
+        assert np.array_equal(_expand(R), want), name
+        assert (R[6] >= R[4]).all() and (R[7] >= R[4]).all()      # forward 2-D patterns
+        if name != "c1":
+            assert len(R[0]) * 100 < len(runs), (name, len(R[0]), len(runs))
+        P.close()

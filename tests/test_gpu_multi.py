@@ -13,12 +13,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(n, full, port):
+def _run(n, full, port, extra=(), env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_worker.py")]
     if full:
         cmd.append("--full")
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200)
+    cmd += list(extra)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200,
+                       env=dict(os.environ, **(env or {})))
     assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-5000:]
 
 
@@ -27,3 +29,12 @@ def test_multi_gpu_parity(n):
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     _run(n, full=(n == max(k for k in (2, 4, 8) if k <= torch.cuda.device_count())), port=29500 + n)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multicast_unicast_split_parity(n):
+    """The opt-in multicast egress split (LLRL_MC_UNICAST_PERIOD=k: every k-th
+    multicast item pushed to each replica as plain peer stores) is bit-exact."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, full=False, port=29520 + n, extra=["--mc-only"], env={"LLRL_MC_UNICAST_PERIOD": "3"})

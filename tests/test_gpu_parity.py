@@ -324,12 +324,15 @@ def test_toy_parity_cast_variants(rt, variant, monkeypatch):
 
 @pytest.mark.parametrize("tmap", ["0", "1"])
 @pytest.mark.parametrize("frac", ["0", "0.5", "1"])
-def test_toy_parity_cast_item_order(rt, tmap, frac, monkeypatch):
-    """The TMA cast launch's item orders (LLRL_STATIC_FRAC: striped share, rest
-    claimed from the queue) and its optional 3-D tensor-map boxes for strided
-    sources (LLRL_CAST_TMAP=1: o / down column bands of FSDP row chunks) are
-    bit-exact, for every cast flavour (bf16, f32, MXFP8, NVFP4)."""
+@pytest.mark.parametrize("block", ["0", "1"])
+def test_toy_parity_cast_item_order(rt, tmap, frac, block, monkeypatch):
+    """The TMA cast launch's item orders (LLRL_STATIC_FRAC: static share, rest
+    claimed from the queue; LLRL_STATIC_BLOCK: static items striped or one block
+    per CTA) and its optional 3-D tensor-map boxes for strided sources
+    (LLRL_CAST_TMAP=1: o / down column bands of FSDP row chunks) are bit-exact,
+    for every cast flavour (bf16, f32, MXFP8, NVFP4)."""
     monkeypatch.setenv("LLRL_STATIC_FRAC", frac)
+    monkeypatch.setenv("LLRL_STATIC_BLOCK", block)
     monkeypatch.setenv("LLRL_CAST_TMAP", tmap)
     for sdt, ddt, f, tt, tg in (("f32", "bf16", 3, 1, 4), ("bf16", "bf16", 4, 1, 2), ("f32", "f32", 2, 1, 2),
                                 ("bf16", "mxfp8", 4, 1, 4), ("f32", "nvfp4", 2, 1, 4)):
