@@ -13,7 +13,9 @@
 #   timeline N CFG       per-CTA start / end spread of the cast launch (tools/timeline.py)
 #   launches CFG         ncu launch list (gpu__time_duration, --clock-control none), 1 GPU
 #   ncufull CFG KERNEL   ncu --set full of one kernel (regex), 1 GPU, 1 launch
-#   nvlink N CFG         ncu NVLink + DRAM counters, one process driving N GPUs
+#   nvlink N CFG         ncu NVLink + DRAM counters, one process driving N GPUs (NVFP4: the
+#                        supplied-amax one-pass sync -- the two-pass handshake would deadlock
+#                        under ncu's serialised launches)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -81,7 +83,7 @@ ncufull)
         --no-cpu-baseline --no-nv-supplied > "gpurun_out/ncufull_${cfg}.log" 2>&1 ;;
 nvlink)
     n=$1; cfg=$2
-    timeout 1500 ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    timeout ${NVL_TIMEOUT:-600} ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
         --clock-control none -k regex:llrl_k_cast --csv --log-file "gpurun_out/nvlink_${cfg}_n${n}.csv" \
         python tools/nvlink_1proc.py "$cfg" "$n" >"gpurun_out/nvlink_${cfg}_n${n}.log" 2>&1 ;;
 *)

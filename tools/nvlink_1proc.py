@@ -49,9 +49,20 @@ def main():
     for d in range(G):
         torch.cuda.synchronize(d)
 
+    # NVFP4: the one-pass sync with a supplied per-tensor amax (llrl_sync_nv_amax).
+    # The two-pass sync's cross-GPU amax handshake waits on other GPUs' kernels,
+    # which ncu's serialisation of the profiled launches would deadlock; the
+    # bytes moved are the same (the amax value only changes the codes)
+    nv = cfg.dst_dtype == "nvfp4"
+    amax = [torch.ones(max(1, plan.nv_num_tensors()), dtype=torch.float32, device=f"cuda:{d}") for d in range(G)] \
+        if nv else None
+
     def one():
         for d in range(G):
-            plan.sync(comms[d], d, sp, dp, streams[d].cuda_stream)
+            if nv:
+                plan.sync_nv_amax(comms[d], d, amax[d].data_ptr(), sp, dp, streams[d].cuda_stream)
+            else:
+                plan.sync(comms[d], d, sp, dp, streams[d].cuda_stream)
 
     one()
     for d in range(G):
