@@ -855,7 +855,8 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
             const int des = mx ? 1 : cast ? 2 : es;
-            char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
+            // F_MC: the position's multicast VA (bulk stores through NVLS, LLRL_MC_TMA=1)
+            char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
             {
                 if (!vec) {                       // scalar item: workers wrote global memory directly
                     if (lane == 0) {
@@ -933,7 +934,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             // static phase: the item and its tensor table were ready before its data
             if (!handoff) mbar_wait(&full_bar[st], (n / kCastStages) & 1);
             const bool dst_f32 = it.flags & F_DST_F32;
-            char *dbase = static_cast<char *>(P.dst[it.dst_rank]);
+            char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
                 const char *src = static_cast<const char *>(P.src[it.src_rank]);
                 const int ne = it.rows * it.cols;

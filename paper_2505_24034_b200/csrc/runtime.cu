@@ -120,7 +120,10 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     }
     if (const char *v = getenv("LLRL_CAST_VARIANT")) W.variant = atoi(v);   // tuning knob
     if (has_mx && W.variant < kCastTmaVariant) W.variant = kCastTmaVariant + 1;   // MX: TMA kernels only
-    if (W.has_mc && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;   // multicast: register kernel
+    // multicast: register kernel (multimem.st); LLRL_MC_TMA=1 keeps the TMA kernel,
+    // whose storer bulk-stores F_MC stages through the multicast VA
+    const char *mct = getenv("LLRL_MC_TMA");
+    if (W.has_mc && !(mct && atoi(mct)) && (W.variant < 0 || W.variant >= kCastTmaVariant)) W.variant = 1;
     if (W.variant < 0 || W.variant >= num_cast_variants()) W.variant = kDefaultCastVariant;
     W.fp8_variant = 1;                                                       // TMA pipeline
     if (const char *v = getenv("LLRL_PDL")) W.no_pdl = atoi(v) == 0;
