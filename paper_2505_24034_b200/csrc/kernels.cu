@@ -667,30 +667,28 @@ __device__ __forceinline__ Chunk cast_chunk(const Item &it, int es, int rows_per
     return c;
 }
 
-// A role's walk over the (item, chunk) stages of its CTA, in two phases.
+// The item sequence of a CTA, which its three roles walk in lockstep, each role
+// looping over an item's chunks (stages) inside its item loop -- per-item work
+// (descriptor load, flags, chunk geometry, NVFP4 tensor table) stays out of the
+// per-stage path, which matters for the quantising variant's 16 KiB stages
+// (two 16-element units per worker thread per stage).
 // Static phase, items [item_begin, static_end): striding (CTA b takes items b,
 // b + gridDim.x, ...) or, with P.static_block, a contiguous block of them per
 // CTA (the plan interleaves destinations in proportion to their bytes, so a
 // block carries every destination's share while a stride can alias with the
-// interleave period: 4 destinations and 148 CTAs give each CTA one
-// destination); every role walks this sequence itself and loads an
-// item's descriptor before it waits for the item's first stage -- no hand-off.
-// Dynamic phase, items [static_end, item_end) (only with P.queue): the producer
+// interleave period); every role walks this sequence itself.
+// Claimed phase, items [static_end, item_end) (only with P.queue): the producer
 // claims each item with one atomicAdd (the next claim in flight while the
-// current item's copies are issued) and hands each stage's item and chunk to
-// the other roles in shared memory.  The dynamic tail absorbs the spread of
-// per-SM speeds, so all CTAs finish together; the static bulk keeps the
-// per-stage hand-off off the critical path.
-struct StageWalk {
-    int i, k, nch, rows_per, segs;
-    int step, static_hi;             // static phase: i += step while i < static_hi
+// current item's copies are issued) and hands the item to the other roles in
+// shared memory at the item's first stage (index -1: end of work).  The claimed
+// tail absorbs the spread of per-SM and per-link speeds, so all CTAs finish
+// together.
+struct ItemWalk {
+    int i, step, static_hi;
     unsigned claimed;
     bool dyn;
-    int band, band_row, band_rows;   // producer: strided-source band map of the item (-1: none)
-    Item it;
 };
-enum { WALK_END = 0, WALK_STAGE = 1, WALK_HANDOFF = 2 };
-__device__ __forceinline__ void walk_init(StageWalk &w, const KParams &P, bool producer, int lane) {
+__device__ __forceinline__ void walk_init(ItemWalk &w, const KParams &P, bool producer, int lane) {
     if (P.static_block) {
         const int64_t n = P.static_end - P.item_begin;
         w.step = 1;
@@ -701,47 +699,24 @@ __device__ __forceinline__ void walk_init(StageWalk &w, const KParams &P, bool p
         w.i = P.item_begin + int(blockIdx.x) - int(gridDim.x);
         w.static_hi = P.static_end;
     }
-    w.k = w.nch = 0;
     w.claimed = 0;
     w.dyn = false;
     if (producer && P.queue && lane == 0) w.claimed = atomicAdd(P.queue, 1u);   // first claim, in flight
 }
-// Next stage of this role: WALK_STAGE (w.it, c set), WALK_END, or -- consumers
-// entering the dynamic phase -- WALK_HANDOFF (read stages from shared memory).
-template <int SB>
-__device__ __forceinline__ int walk_next(StageWalk &w, const KParams &P, int es, bool producer, int lane, Chunk &c) {
-    if (w.k == w.nch) {
-        w.k = 0;
-        if (!w.dyn) {
-            w.i += w.step;
-            if (w.i >= w.static_hi) {
-                if (!P.queue) return WALK_END;
-                w.dyn = true;
-                if (!producer) return WALK_HANDOFF;
-            }
-        }
-        if (w.dyn) {
-            w.i = P.static_end + int(__shfl_sync(0xffffffffu, w.claimed, 0));
-            if (w.i >= P.item_end) return WALK_END;
-            if (lane == 0) w.claimed = atomicAdd(P.queue, 1u);   // the next item, in flight
-        }
-        w.it = P.items[w.i];
-        w.nch = (w.it.flags & F_VEC) ? cast_chunks<SB>(w.it, es, &w.rows_per, &w.segs) : 1;
-        w.band = -1;
-        if (producer && P.cast_refs) {
-            const CastRef r = P.cast_refs[w.i];
-            if (r.map >= 0) {
-                w.band_rows = P.cast_box[r.map];
-                if (w.band_rows > 0) {
-                    w.band = r.map;
-                    w.band_row = r.row;
-                }
-            }
-        }
-    }
-    c = (w.it.flags & F_VEC) ? cast_chunk<SB>(w.it, es, w.rows_per, w.segs, w.k) : Chunk{0, 0, 0, 0};
-    w.k++;
-    return WALK_STAGE;
+// Static phase: the next item (>= 0), or -1 at its end; sets w.dyn when a
+// claimed phase follows.
+__device__ __forceinline__ int walk_static(ItemWalk &w, const KParams &P) {
+    w.i += w.step;
+    if (w.i < w.static_hi) return w.i;
+    w.dyn = P.queue != nullptr;
+    return -1;
+}
+// Producer, claimed phase: the next claimed item, or -1 when the queue is empty.
+__device__ __forceinline__ int walk_claim(ItemWalk &w, const KParams &P, int lane) {
+    const int i = P.static_end + int(__shfl_sync(0xffffffffu, w.claimed, 0));
+    if (i >= P.item_end) return -1;
+    if (lane == 0) w.claimed = atomicAdd(P.queue, 1u);   // the next item, in flight
+    return i;
 }
 
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
@@ -780,21 +755,22 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // dynamic phase: what each stage holds -- item index (-1: end of work), the
-    // item, the chunk -- written by the producer before its arrive (release ->
-    // acquire)
+    // claimed phase: the item (index, -1: end of work; descriptor) each stage
+    // starts, written by the producer before its arrive on the stage's full
+    // barrier (release -> acquire; the storer sees it through the workers' arrive)
     __shared__ int s_item[kCastStages];
     __shared__ Item s_it[kCastStages];
-    __shared__ Chunk s_ch[kCastStages];
-    StageWalk w;
+    ItemWalk w;
     walk_init(w, P, warp == 0, lane);
     if (warp == 0) {
         // producer: stages the rows of every vector item; scalar items pass a token
-        for (int n = 0;; n++) {
-            const int st = n % kCastStages;
-            Chunk c;
-            if (walk_next<SB>(w, P, es, true, lane, c) == WALK_END) {
-                if (P.queue) {                    // end-of-work token for the other roles
+        int n = 0;
+        for (;;) {
+            int i = w.dyn ? -1 : walk_static(w, P);
+            if (i < 0 && w.dyn) i = walk_claim(w, P, lane);
+            if (i < 0) {
+                if (w.dyn) {                      // end-of-work token for the other roles
+                    const int st = n % kCastStages;
                     mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
                     if (lane == 0) {
                         s_item[st] = -1;
@@ -803,61 +779,76 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 }
                 break;
             }
-            const Item &it = w.it;
-            mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
-            if (w.dyn && lane == 0) {
-                s_item[st] = w.i;
-                s_it[st] = it;
-                s_ch[st] = c;
-            }
-            if (!(it.flags & F_VEC)) {
-                if (lane == 0) mbar_arrive(&full_bar[st]);
-                continue;
+            const Item it = P.items[i];
+            const bool vec = it.flags & F_VEC;
+            int rows_per = 1, segs = 1;
+            const int nch = vec ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
+            int band = -1, band_row = 0, band_rows = 0;   // strided-source band map (LLRL_CAST_TMAP)
+            if (P.cast_refs) {
+                const CastRef r = P.cast_refs[i];
+                if (r.map >= 0 && (band_rows = P.cast_box[r.map]) > 0) {
+                    band = r.map;
+                    band_row = r.row;
+                }
             }
             const char *src = static_cast<const char *>(P.src[it.src_rank]) + it.src_off * es;
-            if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
-            __syncwarp();
-            unsigned char *dst = stages + st * kStride;
-            if (c.nc == it.src_ld) {              // rows contiguous in the source: one bulk copy
-                if (lane == 0)
-                    bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
-            } else if (w.band >= 0 && c.nc == it.cols && c.nr == w.band_rows) {
-                // strided whole rows: one 3-D tensor box (the band's map) instead of a copy per row
-                if (lane == 0)
-                    tma_box3_g2s(dst, static_cast<const unsigned char *>(P.cast_tmaps) + 128 * w.band, w.band_row + c.r0,
-                                 &full_bar[st]);
-            } else {
-                for (int r = lane; r < c.nr; r += 32)
-                    bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
-                             uint32_t(c.nc * es), &full_bar[st]);
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                mbar_wait(&empty_bar[st], ((n / kCastStages) & 1) ^ 1);
+                if (w.dyn && k == 0 && lane == 0) {
+                    s_item[st] = i;
+                    s_it[st] = it;
+                }
+                if (!vec) {
+                    if (lane == 0) mbar_arrive(&full_bar[st]);
+                    continue;
+                }
+                const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
+                if (lane == 0) mbar_arrive_tx(&full_bar[st], uint32_t(c.nr * c.nc * es));
+                __syncwarp();
+                unsigned char *dst = stages + st * kStride;
+                if (c.nc == it.src_ld) {          // rows contiguous in the source: one bulk copy
+                    if (lane == 0)
+                        bulk_g2s(dst, src + int64_t(c.r0) * it.src_ld * es, uint32_t(c.nr * c.nc * es), &full_bar[st]);
+                } else if (band >= 0 && c.nc == it.cols && c.nr == band_rows) {
+                    // strided whole rows: one 3-D tensor box (the band's map) instead of a copy per row
+                    if (lane == 0)
+                        tma_box3_g2s(dst, static_cast<const unsigned char *>(P.cast_tmaps) + 128 * band, band_row + c.r0,
+                                     &full_bar[st]);
+                } else {
+                    for (int r = lane; r < c.nr; r += 32)
+                        bulk_g2s(dst + r * c.nc * es, src + (int64_t(c.r0 + r) * it.src_ld + c.c0) * es,
+                                 uint32_t(c.nc * es), &full_bar[st]);
+                }
             }
         }
     } else if (warp == 1) {
         // storer: write each converted stage back, release it once read
-        int pend = -1;
-        bool handoff = false;
-        for (int n = 0;; n++) {
-            const int st = n % kCastStages;
-            Chunk c;
-            if (!handoff) {
-                const int r = walk_next<SB>(w, P, es, false, lane, c);
-                if (r == WALK_END) break;
-                handoff = r == WALK_HANDOFF;
-            }
-            mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
-            if (handoff) {
+        int n = 0, pend = -1;
+        for (;;) {
+            int i = w.dyn ? -1 : walk_static(w, P);
+            Item it;
+            if (i >= 0) {
+                it = P.items[i];
+            } else if (w.dyn) {                   // claimed phase: the item arrives with its first stage
+                const int st = n % kCastStages;
+                mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
                 if (s_item[st] < 0) break;
-                w.it = s_it[st];
-                c = s_ch[st];
+                it = s_it[st];
+            } else {
+                break;
             }
-            const Item &it = w.it;
             const bool vec = it.flags & F_VEC;
+            int rows_per = 1, segs = 1;
+            const int nch = vec ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
             const bool mx = it.flags & F_MX, fp4 = it.flags & F_FP4;
             const bool cast = SRC_F32 && !(it.flags & F_DST_F32) && !mx;
             const int des = mx ? 1 : cast ? 2 : es;
             // F_MC: the position's multicast VA (bulk stores through NVLS, LLRL_MC_TMA=1)
             char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
-            {
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                if (!(w.dyn && k == 0)) mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
                 if (!vec) {                       // scalar item: workers wrote global memory directly
                     if (lane == 0) {
                         // release the deferred stage now: the producer may need it before
@@ -872,6 +863,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                     continue;
                 }
                 if (lane == 0) {
+                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                     const unsigned char *out = stages + st * kStride + ((cast || mx) ? kCastStageBytes : 0);
                     // rows contiguous in the destination (chunk spans whole rows): one bulk store
                     const int nrow = c.nc == it.dst_ld ? 1 : c.nr, nel = c.nc == it.dst_ld ? c.nr * c.nc : c.nc;
@@ -894,48 +886,31 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
     } else {
         // workers
         const int wt = threadIdx.x - 64;
+        int n = 0;
         int nv_tid = -1, nv_buf = 0;
-        bool handoff = false;
-        for (int n = 0;; n++) {
-            const int st = n % kCastStages;
-            Chunk c;
-            if (!handoff) {
-                const int r = walk_next<SB>(w, P, es, false, lane, c);
-                if (r == WALK_END) break;
-                handoff = r == WALK_HANDOFF;
-            }
-            if (handoff) {
+        for (;;) {
+            int i = w.dyn ? -1 : walk_static(w, P);
+            Item it;
+            if (i >= 0) {
+                it = P.items[i];
+            } else if (w.dyn) {                   // claimed phase: the item arrives with its first stage
+                const int st = n % kCastStages;
                 mbar_wait(&full_bar[st], (n / kCastStages) & 1);
                 if (s_item[st] < 0) {             // end of work: pass the token to the storer
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&conv_bar[st]);
                     break;
                 }
-                w.it = s_it[st];
-                c = s_ch[st];
+                it = s_it[st];
+            } else {
+                break;
             }
-            const Item &it = w.it;
-            if ((it.flags & F_NV) && (it.flags & F_VEC) && it.tid != nv_tid) {
-                // R16, per generator tensor: S_enc = 2688 / max(A, 2^-64), and for every
-                // E4M3 group-scale code c the element multiplier r(c) = S_enc / s_q(c)
-                // (0 for s_q = 0) -- one exact division per code instead of per group.
-                // Double-buffered: a worker one tensor ahead writes the other table.
-                nv_tid = it.tid;
-                nv_buf ^= 1;
-                const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
-                const float s_enc = __fdiv_rn(2688.0f, A);
-                if (wt < 128) {
-                    const float sq = e4m3_value(uint32_t(wt));
-                    nv_r[nv_buf][wt] = (wt == 0 || wt == 127) ? 0.0f : __fdiv_rn(s_enc, sq);
-                }
-                if (wt == 0) nv_senc[nv_buf] = s_enc;
-                asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
-            }
-            // static phase: the item and its tensor table were ready before its data
-            if (!handoff) mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+            const bool first_waited = w.dyn;      // chunk 0's full barrier already passed
             const bool dst_f32 = it.flags & F_DST_F32;
             char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
+                const int st = n % kCastStages;
+                if (!first_waited) mbar_wait(&full_bar[st], (n / kCastStages) & 1);
                 const char *src = static_cast<const char *>(P.src[it.src_rank]);
                 const int ne = it.rows * it.cols;
                 for (int e = wt; e < ne; e += kCastWorkers) {
@@ -952,15 +927,38 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
+                n++;
                 continue;
             }
+            int rows_per, segs;
+            const int nch = cast_chunks<SB>(it, es, &rows_per, &segs);
             const bool mx = it.flags & F_MX;
             const bool fp4 = it.flags & F_FP4;
+            const bool nv = it.flags & F_NV;
             const bool cast = SRC_F32 && !dst_f32 && !mx;
-            {
+            if (nv && it.tid != nv_tid) {
+                // R16, per generator tensor: S_enc = 2688 / max(A, 2^-64), and for every
+                // E4M3 group-scale code c the element multiplier r(c) = S_enc / s_q(c)
+                // (0 for s_q = 0) -- one exact division per code instead of per group.
+                // Double-buffered: a worker one tensor ahead writes the other table.
+                nv_tid = it.tid;
+                nv_buf ^= 1;
+                const float A = fmaxf(__uint_as_float(P.nv_amax[it.tid]), 0x1p-64f);
+                const float s_enc = __fdiv_rn(2688.0f, A);
+                if (wt < 128) {
+                    const float sq = e4m3_value(uint32_t(wt));
+                    nv_r[nv_buf][wt] = (wt == 0 || wt == 127) ? 0.0f : __fdiv_rn(s_enc, sq);
+                }
+                if (wt == 0) nv_senc[nv_buf] = s_enc;
+                asm volatile("bar.sync 1, %0;" ::"n"(NWK) : "memory");
+            }
+            for (int k = 0; k < nch; k++, n++) {
+                const int st = n % kCastStages;
+                if (!(first_waited && k == 0)) mbar_wait(&full_bar[st], (n / kCastStages) & 1);
                 unsigned char *in = stages + st * kStride;
                 unsigned char *out = in + kCastStageBytes;
                 if (cast || mx) {
+                    const Chunk c = cast_chunk<SB>(it, es, rows_per, segs, k);
                     if (cast) {
                         const int nunits = c.nr * c.nc / 4;          // 4 fp32 -> 4 bf16 per unit
                         for (int u = wt; u < nunits; u += kCastWorkers) {
@@ -970,7 +968,6 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                            bf16x2_rn(__uint_as_float(a.z), __uint_as_float(a.w)));
                         }
                     } else {
-                        const bool nv = it.flags & F_NV;
                         // MX (R13 / R15): lanes (2j, 2j+1) hold the two halves of one 1x32 group;
                         // NVFP4 (R16): each thread's 16 elements are one 1x16 group
                         const int nunits = c.nr * c.nc / 16;         // 16 elements per thread
@@ -985,16 +982,16 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             const int u = u0 + wt;
                             const bool live = u < nunits;
                             constexpr int W = SRC_F32 ? 4 : 2;
-                            uint4 w[W];
+                            uint4 wd[W];
                             uint32_t amax = 0;
 #pragma unroll
                             for (int j = 0; j < W; j++)
-                                w[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
+                                wd[j] = live ? reinterpret_cast<const uint4 *>(in + u * 16 * es)[j] : make_uint4(0, 0, 0, 0);
                             if (SRC_F32) {
 #pragma unroll
-                                for (int j = 0; j < W; j++) amax = word_amax<SRC_F32>(w[j], amax);
+                                for (int j = 0; j < W; j++) amax = word_amax<SRC_F32>(wd[j], amax);
                             } else {
-                                amax = amax16_bf16(w[0], w[W - 1]);
+                                amax = amax16_bf16(wd[0], wd[W - 1]);
                             }
                             if (nv) {
                                 // group scale s = (amax / 6) * S_enc -> E4M3 code; r = S_enc / s_q
@@ -1002,7 +999,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                                 const uint32_t sc = e4m3x2_rn(__fmul_rn(t6, nv_senc[nv_buf]), 0.0f) & 0xFFu;
                                 const float r = nv_r[nv_buf][sc];
                                 if (live) {
-                                    reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, r);
+                                    reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(wd, r);
                                     // scale byte: sb[u], plus gap per chunk row (dst_off, dst_ld, c0: whole groups)
                                     int g = u;
                                     if (gap) g += __float2int_rz((float(u) + 0.5f) * inv_upr) * gap;
@@ -1016,8 +1013,8 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                             const int code = max(int(amax >> 23) - (fp4 ? 2 : 8), 0);
                             const float inv = __uint_as_float(uint32_t(254 - code) << 23);   // 2^-(code - 127)
                             if (live) {
-                                if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(w, inv);
-                                else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(w, inv);
+                                if (fp4) reinterpret_cast<uint2 *>(out)[u] = quant16_e2m1<SRC_F32, W>(wd, inv);
+                                else reinterpret_cast<uint4 *>(out)[u] = quant16<SRC_F32, W>(wd, inv);
                                 if ((u & 1) == 0) {   // group index as for NVFP4, 32-element groups
                                     int g = u >> 1;
                                     if (gap) g += __float2int_rz((float(u) + 0.5f) * inv_upr) * gap;
