@@ -823,21 +823,13 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             }
         }
     } else if (warp == 1) {
-        // storer: write each converted stage back, release it once read
+        // storer: write each converted stage back, release it once read.  One item
+        // body, inlined into the static loop (item from the plan table) and into
+        // the claimed loop (item handed over in shared memory, its first stage's
+        // barrier already passed).  The item is taken BY VALUE: its shared-memory
+        // slot is rewritten once the producer recycles the item's first stage.
         int n = 0, pend = -1;
-        for (;;) {
-            int i = w.dyn ? -1 : walk_static(w, P);
-            Item it;
-            if (i >= 0) {
-                it = P.items[i];
-            } else if (w.dyn) {                   // claimed phase: the item arrives with its first stage
-                const int st = n % kCastStages;
-                mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
-                if (s_item[st] < 0) break;
-                it = s_it[st];
-            } else {
-                break;
-            }
+        auto item = [&](const Item it, const bool first_waited) {
             const bool vec = it.flags & F_VEC;
             int rows_per = 1, segs = 1;
             const int nch = vec ? cast_chunks<SB>(it, es, &rows_per, &segs) : 1;
@@ -848,7 +840,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
             char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
             for (int k = 0; k < nch; k++, n++) {
                 const int st = n % kCastStages;
-                if (!(w.dyn && k == 0)) mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
+                if (!(first_waited && k == 0)) mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
                 if (!vec) {                       // scalar item: workers wrote global memory directly
                     if (lane == 0) {
                         // release the deferred stage now: the producer may need it before
@@ -878,34 +870,25 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                     pend = st;
                 }
             }
+        };
+        for (int i; (i = walk_static(w, P)) >= 0;) item(P.items[i], false);
+        while (w.dyn) {                           // claimed phase: the item arrives with its first stage
+            const int st = n % kCastStages;
+            mbar_wait(&conv_bar[st], (n / kCastStages) & 1);
+            if (s_item[st] < 0) break;
+            item(s_it[st], true);
         }
         if (lane == 0) {
             bulk_wait_all();                      // every bulk store complete before the signal
             if (pend >= 0) mbar_arrive(&empty_bar[pend]);
         }
     } else {
-        // workers
+        // workers: one item body, inlined into the static and the claimed loop (as
+        // for the storer)
         const int wt = threadIdx.x - 64;
         int n = 0;
         int nv_tid = -1, nv_buf = 0;
-        for (;;) {
-            int i = w.dyn ? -1 : walk_static(w, P);
-            Item it;
-            if (i >= 0) {
-                it = P.items[i];
-            } else if (w.dyn) {                   // claimed phase: the item arrives with its first stage
-                const int st = n % kCastStages;
-                mbar_wait(&full_bar[st], (n / kCastStages) & 1);
-                if (s_item[st] < 0) {             // end of work: pass the token to the storer
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&conv_bar[st]);
-                    break;
-                }
-                it = s_it[st];
-            } else {
-                break;
-            }
-            const bool first_waited = w.dyn;      // chunk 0's full barrier already passed
+        auto item = [&](const Item it, const bool first_waited) {
             const bool dst_f32 = it.flags & F_DST_F32;
             char *dbase = static_cast<char *>((it.flags & F_MC) ? P.dst_mc[it.dst_rank] : P.dst[it.dst_rank]);
             if (!(it.flags & F_VEC)) {
@@ -928,7 +911,7 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
                 n++;
-                continue;
+                return;
             }
             int rows_per, segs;
             const int nch = cast_chunks<SB>(it, es, &rows_per, &segs);
@@ -1028,6 +1011,17 @@ __global__ void __launch_bounds__(64 + NWK, MINB) llrl_k_cast_tma(const __grid_c
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&conv_bar[st]);
             }
+        };
+        for (int i; (i = walk_static(w, P)) >= 0;) item(P.items[i], false);
+        while (w.dyn) {                           // claimed phase: the item arrives with its first stage
+            const int st = n % kCastStages;
+            mbar_wait(&full_bar[st], (n / kCastStages) & 1);
+            if (s_item[st] < 0) {                 // end of work: pass the token to the storer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv_bar[st]);
+                break;
+            }
+            item(s_it[st], true);
         }
     }
     complete(P);

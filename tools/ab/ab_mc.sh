@@ -8,10 +8,4 @@ for t in 0 1; do
   LLRL_MC_TMA=$t timeout 180 $R --nproc-per-node 4 --master-port $((29810 + t)) bench.py --gpus 4 --config c9 --multicast --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>/tmp/err.txt | tail -1 > /tmp/o.json
   python -c "import json;d=json.loads(open('/tmp/o.json').read());print('mc_tma=$t c9', d['value'], d['ms_min'], d['roofline']['frac'], d['clocks']['reasons'])" || tail -3 /tmp/err.txt
 done
-for f in 1 0; do
-  for cfg in c3 c12; do
-    LLRL_STAGE_FILL=$f timeout 180 $R --nproc-per-node 4 --master-port $((29820 + f)) bench.py --gpus 4 --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>/tmp/err.txt | tail -1 > /tmp/o.json
-    python -c "import json;d=json.loads(open('/tmp/o.json').read());print('fill=$f n=4 $cfg', d['value'], d['ms_min'], d['roofline']['frac'], d.get('nvfp4_supplied_amax',{}).get('value'), d['clocks']['reasons'])" || tail -3 /tmp/err.txt
-  done
-done
 NVL_TIMEOUT=240 bash tools/gpu.sh nvlink 4 c12; tail -2 gpurun_out/nvlink_c12_n4.log; grep -c llrl_k_cast gpurun_out/nvlink_c12_n4.csv
