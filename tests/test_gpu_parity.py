@@ -341,6 +341,25 @@ def test_toy_parity_cast_item_order(rt, tmap, frac, block, monkeypatch):
         job.close()
 
 
+@pytest.mark.parametrize("variant", ["6", "7"])
+@pytest.mark.parametrize("frac", ["0", "1"])
+def test_long_items_claimed_phase(rt, variant, frac):
+    """Items of many more stages than the ring holds (LLRL_CHUNK_ELEMS = 128 Ki
+    elements: up to 32 stages), claimed or static, in a fresh process
+    (tests/long_items_worker.py): every generator byte equals the oracle's.
+    Guards the claimed phase's hand-off (a consumer must keep its own copy of
+    the item: the producer recycles the item's first stage while the consumer
+    is still on later chunks)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LLRL_CHUNK_ELEMS="131072", LLRL_STATIC_FRAC=frac, LLRL_CAST_VARIANT=variant)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "long_items_worker.py")], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "LONG_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_toy_parity_fp8_variants(rt, variant, monkeypatch):
     """Both fp8 kernels (register / TMA-pipelined, LLRL_FP8_VARIANT) are bit-exact,
