@@ -13,6 +13,10 @@
 #   timeline N CFG       per-CTA start / end spread of the cast launch (tools/timeline.py)
 #   launches CFG         ncu launch list (gpu__time_duration, --clock-control none), 1 GPU
 #   ncufull CFG KERNEL   ncu --set full of one kernel (regex), 1 GPU, 1 launch
+#   final1               end-of-round evidence on 1 GPU: tests + smoke, the default bench
+#                        line, the 1-GPU table, the C2 launch list and ncu capture
+#   final4               end-of-round evidence on 4 GPUs: multi-GPU parity (2 and 4), the
+#                        4-GPU table incl. C9 three ways, the default bench at 1, 2, 4
 #   nvlink N CFG         ncu NVLink + DRAM counters, one process driving N GPUs (NVFP4: the
 #                        supplied-amax one-pass sync -- the two-pass handshake would deadlock
 #                        under ncu's serialised launches)
@@ -86,6 +90,31 @@ nvlink)
     timeout ${NVL_TIMEOUT:-600} ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
         --clock-control none -k regex:llrl_k_cast --csv --log-file "gpurun_out/nvlink_${cfg}_n${n}.csv" \
         python tools/nvlink_1proc.py "$cfg" "$n" >"gpurun_out/nvlink_${cfg}_n${n}.log" 2>&1 ;;
+final1)
+    rev=$(cat .git_rev 2>/dev/null || echo snapshot)
+    bash "$0" tests
+    sed -i "s/(snapshot)/($rev)/" gpurun_out/pytest_gpu.log
+    timeout 900 python bench.py > gpurun_out/final_bench_n1.json 2> gpurun_out/final_bench_n1.err
+    bash "$0" table 1 c1 c2 c3 c4 c7 c10 c11 c12 > gpurun_out/final_table_n1.txt 2>&1
+    bash "$0" launches c2
+    bash "$0" ncufull c2 llrl_k_cast_tma
+    ncu -i gpurun_out/ncu_c2_llrl_k_cast_tma.ncu-rep --page raw --csv > gpurun_out/ncu_c2_raw.csv 2>/dev/null
+    timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/final_ref_n1.json 2> gpurun_out/final_ref_n1.err
+    echo "final1 done ($rev)" ;;
+final4)
+    rev=$(cat .git_rev 2>/dev/null || echo snapshot)
+    timeout 1500 python -m pytest tests/test_gpu_multi.py -m gpu -q -rs > gpurun_out/pytest_multi.log 2>&1
+    echo "pytest rc=$? ($rev)" >> gpurun_out/pytest_multi.log
+    bash "$0" table 4 c2 c3 c4 c5 c6 c7 c8 c10 c11 c12 > gpurun_out/final_table_n4.txt 2>&1
+    for extra in "--multicast" "--step-sync" "--replicate nccl --step-sync"; do
+        port=$((port + 1))
+        tag=$(echo $extra | tr -d ' -')
+        timeout 600 $R --nproc-per-node 4 --master-port $port bench.py --gpus 4 --config c9 $extra --steps 10 \
+            --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/table_c9_${tag}_n4.json" 2> /dev/null
+        tail -c 300 "gpurun_out/table_c9_${tag}_n4.json" >> gpurun_out/final_table_n4.txt
+    done
+    bash "$0" scale 4
+    echo "final4 done ($rev)" ;;
 *)
     echo "unknown recipe $recipe"; exit 2 ;;
 esac
