@@ -140,18 +140,18 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     }
     CK(cudaMalloc(&W.d_queue, 256));
     CK(cudaMemset(W.d_queue, 0, 256));
-    // Item order of the TMA cast launch (kernels.cu StageWalk): the first
+    // Item order of the TMA cast launch (kernels.cu ItemWalk): the first
     // static_frac of a launch's items striped over the CTAs, the rest claimed
-    // dynamically.  Striping is cheaper per stage (no shared-memory hand-off);
-    // the claimed tail lets every CTA finish together whatever its SM's speed.
-    // Measured (profiles/r02/ab/): with pushes to peer GPUs,
-    // all claimed (C3 13.13 vs 13.88 ms at 0.9 striped, C8 29.24 vs 30.66, C2
-    // 11.20 vs 11.43 at 4 GPUs: a CTA's share of each link follows the plan's
-    // interleave, whatever the per-link speeds); local-only syncs: 0.9 is
-    // within noise of the best on C2, C3, C11, C12 at 1 GPU, and plans with an
-    // fp8 launch behind the cast launch (C4) run 7% faster fully striped --
-    // CTAs that finish early hand their SM to the programmatically dependent
-    // fp8 grid.
+    // dynamically.  Striped items need no hand-off (each role reads the plan
+    // table itself); the claimed tail lets every CTA finish together whatever
+    // its SM's speed.  Measured (profiles/r02/ab/): with
+    // pushes to peer GPUs, all claimed (C3 13.13 vs 13.88 ms at 0.9 striped, C8
+    // 29.24 vs 30.66, C2 11.20 vs 11.43 at 4 GPUs: a CTA's share of each link
+    // follows the plan's interleave, whatever the per-link speeds); local-only
+    // syncs: 0.9 (C3 21.5 vs 22.2 ms fully striped, C10 16.2 vs 16.5), and
+    // plans with an fp8 launch behind the cast launch (C4) run 7% faster fully
+    // striped -- CTAs that finish early hand their SM to the programmatically
+    // dependent fp8 grid.
     bool pushes_remote = false;
     for (int64_t i = 0; i < n_cast && !pushes_remote; i++)
         pushes_remote = p->dst_device[size_t(W.items[size_t(i)].dst_rank)] != device;

@@ -413,9 +413,15 @@ def test_toy_parity_overlapped_step(rt, sdt, ddt):
 
 
 @pytest.mark.parametrize("sdt,ddt", [("f32", "bf16"), ("bf16", "fp8"), ("bf16", "mxfp8")])
-def test_toy_parity_cuda_graph_replay(rt, sdt, ddt):
+@pytest.mark.parametrize("kernel", ["default", "tma-claimed"])
+def test_toy_parity_cuda_graph_replay(rt, sdt, ddt, kernel, monkeypatch):
     """Completion state lives on the device, so a warmed-up sync (and the per-layer
-    overlapped step) can be captured once in a CUDA graph and replayed."""
+    overlapped step) can be captured once in a CUDA graph and replayed -- also
+    through the TMA cast kernel with every item claimed from its queue (the last
+    CTA out resets the queue for the next launch / replay)."""
+    if kernel == "tma-claimed":
+        monkeypatch.setenv("LLRL_CAST_VARIANT", "6")
+        monkeypatch.setenv("LLRL_STATIC_FRAC", "0")
     job = _toy_job(rt, "toy", 2, 2, 4, sdt, ddt)
     ol = oracle.Layout(job.model, 2, 2, 4, sdt, ddt)
     job.sync()                                   # warm-up: uploads tables, encodes tensor maps
