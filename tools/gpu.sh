@@ -105,6 +105,9 @@ final4)
     rev=$(cat .git_rev 2>/dev/null || echo snapshot)
     timeout 1500 python -m pytest tests/test_gpu_multi.py -m gpu -q -rs > gpurun_out/pytest_multi.log 2>&1
     echo "pytest rc=$? ($rev)" >> gpurun_out/pytest_multi.log
+    timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "graph_replay or long_items or item_order" \
+        >> gpurun_out/pytest_multi.log 2>&1
+    echo "pytest (1-GPU subset) rc=$? ($rev)" >> gpurun_out/pytest_multi.log
     bash "$0" table 4 c2 c3 c4 c5 c6 c7 c8 c10 c11 c12 > gpurun_out/final_table_n4.txt 2>&1
     for extra in "--multicast" "--step-sync" "--replicate nccl --step-sync"; do
         port=$((port + 1))
