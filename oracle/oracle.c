@@ -446,8 +446,10 @@ static int check_model(const orc_model *m, const orc_cfg *c)
     if (m->with_embed && m->vocab % T) return ORC_E_INDIVISIBLE;
     /* R15: MXFP4 packs two elements per byte: every quantised generator tensor has
      * an even number of columns (and, for whole 1x32 groups, a multiple of 32);
-     * R16 likewise with 1x16 groups.  Checked after the divisibility rules (a
-     * layout that violates both reports INDIVISIBLE, as the library does). */
+     * R16 likewise with 1x16 groups.  Checked after the divisibility rules
+     * (DESIGN R21: these rules are stated on the generator-local column counts,
+     * which exist only once the split divides; a layout that violates both
+     * reports INDIVISIBLE). */
     if (c->dst_dtype == ORC_MXFP4 && (m->d_model % 32 || (m->n_heads * m->head_dim / c->tp_gen) % 32 ||
                                       (m->d_ffn / c->tp_gen) % 32))
         return ORC_E_UNSUPPORTED;
