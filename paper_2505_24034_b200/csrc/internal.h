@@ -227,6 +227,7 @@ struct DeviceWork {
     unsigned int *d_queue = nullptr;            // dynamic item queue of the TMA cast launch
     double static_frac = 0.9;                   // TMA cast launches: share of items striped (rest claimed)
     int static_block = 0;                       // ... as one contiguous block per CTA instead of a stride
+    int nv_run = 0;                             // NVFP4 amax pass: items per run striped over CTAs (0: one range per CTA)
     void *h2d_stream = nullptr, *d2h_stream = nullptr;   // llrl_sync_host pipeline (cudaStream_t)
     std::vector<void *> events;                           // cudaEvent_t pool for the pipeline
     int64_t n_cast = 0;                // items [0, n_cast) are K_CAST, the rest fp8

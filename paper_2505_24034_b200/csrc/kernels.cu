@@ -1059,12 +1059,15 @@ __global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_nv_amax(const __grid_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int per = (P.n_items + gridDim.x - 1) / gridDim.x;
-    const int i0 = blockIdx.x * per, i1 = min(P.n_items, i0 + per);
+    // Each CTA takes one contiguous item range (P.run = 0, the default) or runs of
+    // P.run items striped over the CTAs (LLRL_NV_RUN; a run is mostly one tensor,
+    // so one atomic per warp per run either way).
+    const int run = P.run > 0 ? P.run : (P.n_items + gridDim.x - 1) / gridDim.x;
     if (warp == kThreads / 32) {
         // producer
         int n = 0;
-        for (int i = i0; i < i1; i++) {
+        for (int r0 = blockIdx.x * run; r0 < P.n_items; r0 += gridDim.x * run)
+        for (int i = r0, i1 = min(P.n_items, r0 + run); i < i1; i++) {
             const Item it = P.items[i];
             if (!(it.flags & F_NV)) continue;
             int rows_per, segs;
@@ -1091,7 +1094,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) llrl_k_nv_amax(const __grid_
         // reducers
         uint32_t amax = 0;
         int cur = -1, n = 0;
-        for (int i = i0; i < i1; i++) {
+        for (int r0 = blockIdx.x * run; r0 < P.n_items; r0 += gridDim.x * run)
+        for (int i = r0, i1 = min(P.n_items, r0 + run); i < i1; i++) {
             const Item it = P.items[i];
             if (!(it.flags & F_NV)) continue;
             if (it.tid != cur) {

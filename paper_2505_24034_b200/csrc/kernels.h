@@ -44,6 +44,7 @@ int cast_stage_bytes(int variant);     // stage bytes of a TMA cast variant
 struct NvAmaxParams {
     const Item *items;
     int n_items;                       // scan items [0, n_items) (the cast range), F_NV ones count
+    int run;                           // items per run, runs striped over the CTAs (0: one range per CTA)
     uint32_t *partial;                 // [n_tensors] local partial amax
     unsigned long long *done;          // self-resetting CTA counter
     const int32_t *contrib;            // tensor ids this device contributes to

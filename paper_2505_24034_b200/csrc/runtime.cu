@@ -163,6 +163,12 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     W.static_block = has_mx ? 1 : 0;
     if (const char *v = getenv("LLRL_STATIC_FRAC")) W.static_frac = std::min(1.0, std::max(0.0, atof(v)));
     if (const char *v = getenv("LLRL_STATIC_BLOCK")) W.static_block = atoi(v) != 0;
+    // NVFP4 amax pass: one contiguous item range per CTA; LLRL_NV_RUN=k stripes
+    // runs of k items over the CTAs instead (kernels.cu llrl_k_nv_amax): k = 32
+    // speeds C12's amax pass 2.6% but slows C11's, the whole syncs -0.8% / +0.8%
+    // (profiles/r02/ab/nv_amax_runs.txt), so the default stays one range
+    W.nv_run = 0;
+    if (const char *v = getenv("LLRL_NV_RUN")) W.nv_run = std::max(0, atoi(v));
     if (const char *v = getenv("LLRL_TIMELINE"))
         if (atoi(v) && W.grid_cast > 0) {
             CK(cudaMalloc(&W.d_timeline, size_t(W.grid_cast) * 16));
@@ -451,6 +457,7 @@ static llrl_status nv_handshake(llrl_plan *p, DeviceWork &W, llrl_comm *comm, in
         std::memset(&a, 0, sizeof a);
         a.items = W.d_items;
         a.n_items = int(W.n_cast);
+        a.run = W.nv_run;
         a.partial = W.d_nv_partial;
         a.done = W.d_nv_done;
         a.contrib = W.d_nv_contrib;

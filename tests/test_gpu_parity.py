@@ -341,6 +341,19 @@ def test_toy_parity_cast_item_order(rt, tmap, frac, block, monkeypatch):
         job.close()
 
 
+@pytest.mark.parametrize("run", ["0", "1", "7", "32"])
+def test_toy_parity_nv_amax_runs(rt, run, monkeypatch):
+    """NVFP4 amax pass with its items split into runs striped over the CTAs
+    (LLRL_NV_RUN; 0 = one range per CTA, the default): bit-exact, including
+    tensors whose items are spread over many CTAs (per-tensor amax combined by
+    atomicMax)."""
+    monkeypatch.setenv("LLRL_NV_RUN", run)
+    for sdt, f, tt, tg in (("bf16", 2, 2, 8), ("f32", 3, 1, 4), ("bf16", 8, 1, 8)):
+        job = _toy_job(rt, "toy", f, tt, tg, sdt, "nvfp4")
+        _run_and_compare(rt, job, seed=int(run) + 5)
+        job.close()
+
+
 @pytest.mark.parametrize("variant", ["6", "7"])
 @pytest.mark.parametrize("frac", ["0", "1"])
 def test_long_items_claimed_phase(rt, variant, frac):
