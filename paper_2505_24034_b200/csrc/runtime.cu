@@ -152,10 +152,20 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     // plans with an fp8 launch behind the cast launch (C4) run 7% faster fully
     // striped -- CTAs that finish early hand their SM to the programmatically
     // dependent fp8 grid.
+    // Quantising syncs that push but are HBM-bound (the device's plan bytes over
+    // the HBM rate exceed its NVLink bytes over the peer-copy rate; C12 at 2 and
+    // 4 GPUs: 2.6 GB over NVLink, 43 GB through HBM per GPU at 4) keep the
+    // local-only order: 13.03 vs 13.91 ms all claimed at 4 GPUs, supplied amax
+    // 7.96 vs 8.80 (profiles/r02/ab/c12_4gpu_order.txt); NVLink-bound syncs
+    // lose with it (C3 at 4 GPUs 13.63 vs 13.14 ms) and plain casts that push
+    // keep claiming (C3 at 2 GPUs, HBM-bound: 20.92 ms claimed).
     bool pushes_remote = false;
     for (int64_t i = 0; i < n_cast && !pushes_remote; i++)
         pushes_remote = p->dst_device[size_t(W.items[size_t(i)].dst_rank)] != device;
-    W.static_frac = pushes_remote ? 0.0 : n_fp8 > 0 ? 1.0 : 0.9;
+    const double t_nvl = double(std::max(W.nvl_tx, W.nvl_rx)) / 770e9,
+                 t_hbm = double(W.hbm_read + W.hbm_write) / 6533e9;   // measured peer copy / HBM copy rates
+    const bool nvlink_bound = pushes_remote && t_nvl > t_hbm;
+    W.static_frac = (pushes_remote && (nvlink_bound || !has_mx)) ? 0.0 : n_fp8 > 0 ? 1.0 : 0.9;
     // Static items of quantising (MX / NVFP4) plans as one contiguous block per
     // CTA: consecutive items then share their generator tensor and tile (fewer
     // NVFP4 table rebuilds, each a barrier across the workers): C7 / C10 / C11 /
