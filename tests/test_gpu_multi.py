@@ -32,9 +32,13 @@ def test_multi_gpu_parity(n):
 
 
 @pytest.mark.parametrize("n", [2, 4])
-def test_multicast_unicast_split_parity(n):
-    """The opt-in multicast egress split (LLRL_MC_UNICAST_PERIOD=k: every k-th
-    multicast item pushed to each replica as plain peer stores) is bit-exact."""
+@pytest.mark.parametrize("mode", ["split", "tma"])
+def test_multicast_opt_in_paths_parity(n, mode):
+    """The opt-in multicast paths are bit-exact: the egress split
+    (LLRL_MC_UNICAST_PERIOD=k: every k-th multicast item pushed to each replica
+    as plain peer stores) and the TMA cast kernel feeding NVLS through its bulk
+    storer (LLRL_MC_TMA=1)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    _run(n, full=False, port=29520 + n, extra=["--mc-only"], env={"LLRL_MC_UNICAST_PERIOD": "3"})
+    env = {"LLRL_MC_UNICAST_PERIOD": "3"} if mode == "split" else {"LLRL_MC_TMA": "1"}
+    _run(n, full=False, port=29520 + n + (10 if mode == "tma" else 0), extra=["--mc-only"], env=env)
