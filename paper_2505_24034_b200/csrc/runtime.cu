@@ -173,11 +173,17 @@ llrl_status ensure_uploaded(llrl_plan *p, int device) {
     W.static_block = has_mx ? 1 : 0;
     if (const char *v = getenv("LLRL_STATIC_FRAC")) W.static_frac = std::min(1.0, std::max(0.0, atof(v)));
     if (const char *v = getenv("LLRL_STATIC_BLOCK")) W.static_block = atoi(v) != 0;
-    // NVFP4 amax pass: one contiguous item range per CTA; LLRL_NV_RUN=k stripes
-    // runs of k items over the CTAs instead (kernels.cu llrl_k_nv_amax): k = 32
-    // speeds C12's amax pass 2.6% but slows C11's, the whole syncs -0.8% / +0.8%
-    // (profiles/r02/ab/nv_amax_runs.txt), so the default stays one range
+    // NVFP4 amax pass: one contiguous item range per CTA, or -- when quantised
+    // sources arrive as strided rows (FSDP chunks into column-split tensors,
+    // C12) -- runs of 32 items striped over the CTAs, so that no CTA's range is
+    // heavy in the slower strided rows (kernels.cu llrl_k_nv_amax): C12's amax
+    // pass 2.6% faster, its sync 0.8%, while contiguous plans (C11) lose 0.8%
+    // with runs (profiles/r02/ab/nv_amax_runs.txt).  LLRL_NV_RUN=k overrides.
     W.nv_run = 0;
+    for (int64_t i = 0; i < n_cast; i++) {
+        const Item &it = W.items[size_t(i)];
+        if ((it.flags & F_NV) && it.rows > 1 && it.cols != it.src_ld) { W.nv_run = 32; break; }
+    }
     if (const char *v = getenv("LLRL_NV_RUN")) W.nv_run = std::max(0, atoi(v));
     if (const char *v = getenv("LLRL_TIMELINE"))
         if (atoi(v) && W.grid_cast > 0) {
